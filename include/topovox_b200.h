@@ -1,0 +1,179 @@
+/*
+ * topovox_b200.h -- C-ABI of the B200-native voxel FEA hot path
+ * (libtopovox_b200.so, sm_100a).
+ *
+ * This is the drop-in boundary for the reference package `topovox`
+ * (/root/reference/pkg/src/topovox). Each entry point names the reference
+ * function it replaces. Conventions:
+ *   - every pointer argument named d_* is DEVICE memory owned by the caller;
+ *     h_* arguments are host memory; nothing here allocates device memory
+ *     except the solve drivers' internal CUDA graph objects;
+ *   - node vectors are f64[3*Nn] interleaved per node (reference numbering,
+ *     topovox/mesh.py:3-6), element vectors are f64[Ne];
+ *   - d_nflags is a u8[Nn] node flag array: bit a (0..2) = DOF 3n+a fixed,
+ *     bit 3 = structural node (built by tvb_node_flags);
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream); calls are
+ *     stream-ordered and asynchronous unless stated otherwise;
+ *   - every call returns a status code (TVB_OK = 0); reductions are
+ *     deterministic (fixed-order two-stage trees, no float atomics).
+ */
+#ifndef TOPOVOX_B200_H
+#define TOPOVOX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (mapped to topovox/errors.py exception types by the Python host) */
+#define TVB_OK 0
+#define TVB_BAD_DIMS 1        /* DimensionMismatch / BadDimension */
+#define TVB_CUDA_ERROR 2
+#define TVB_NOT_SPD 3         /* coarse matrix not SPD (topovox/fea.py:202-205) */
+#define TVB_NO_CONVERGENCE 4  /* NoConvergence (topovox/fea.py:292-297) */
+#define TVB_SINGULAR 5        /* SingularSystem (topovox/fea.py:246-247) */
+#define TVB_BAD_ARG 6
+#define TVB_WORKSPACE 7       /* workspace too small */
+
+/* matvec flags */
+#define TVB_MASK_IN 1     /* zero fixed DOFs of u before applying (fea.py:55-57) */
+#define TVB_MASK_OUT 2    /* zero fixed DOFs of the result (fea.py:63-64) */
+#define TVB_ACCUMULATE 4  /* out += K u (numba seam semantics) instead of out = K u */
+
+int tvb_version(void);
+const char* tvb_last_error(void);
+
+/* Element stiffness k0 (24x24 row-major, host) -> the 45 mode-space
+ * coefficients the matvec consumes. Fails (TVB_BAD_ARG) if k0 is not the
+ * stiffness of an isotropic cube (the mode pattern check). Host only. */
+int tvb_modal_from_k0(const double* h_k0, double* h_mh45);
+
+/* a3: K.u  -- replaces apply_block24 (topovox/backends/numba_kernels.py:12-28)
+ * as called by StiffnessOperator.apply (topovox/fea.py:49-65).
+ * d_dot (optional, device scalar) receives sum(u_masked . out) over all nodes.
+ * d_ws: workspace of tvb_matvec_ws_bytes() bytes (NULL allowed when d_dot is NULL). */
+size_t tvb_matvec_ws_bytes(int nx, int ny, int nz);
+int tvb_matvec(int nx, int ny, int nz, const double* h_mh45, const double* d_u, double* d_out,
+               const double* d_occ, const uint8_t* d_nflags, int flags, double* d_dot, void* d_ws,
+               size_t ws_bytes, void* stream);
+
+/* apply_block24_subset (numba_kernels.py:31-46): out += K_subset u using only
+ * the listed elements (duplicates count with multiplicity). d_ws: f64[Ne] + i32[Ne]. */
+int tvb_matvec_subset(int nx, int ny, int nz, const double* h_mh45, const double* d_u, double* d_out,
+                      const long long* d_elems, long long n_elems_listed, const double* d_occ, void* d_ws,
+                      size_t ws_bytes, void* stream);
+
+/* a4: diag(K) -- replaces diag_block24 (numba_kernels.py:49-58) as used by
+ * StiffnessOperator.diagonal (fea.py:78-85). h_kdiag3 = k0[a,a] for a=0..2.
+ * d_diag (optional) receives the diagonal (accumulated if accumulate != 0);
+ * d_inv (optional) receives 1/diag on free DOFs and 0 on fixed DOFs;
+ * d_zero_free (optional, device int) is incremented for every free DOF with
+ * a zero diagonal. */
+int tvb_diag(int nx, int ny, int nz, const double* d_occ, const uint8_t* d_nflags, const double* h_kdiag3,
+             double* d_diag, int accumulate, double* d_inv, int* d_zero_free, void* stream);
+
+/* node flags from the sorted fixed-DOF list and the occupancy (structural
+ * nodes touch an element with occupancy == 1.0, fea.py:119-123). */
+int tvb_node_flags(int nx, int ny, int nz, const long long* d_fixed_dofs, long long n_fixed, const double* d_occ,
+                   uint8_t* d_nflags, void* stream);
+
+/* deterministic dot product a.b (optionally weighted) -> *d_out */
+size_t tvb_reduce_ws_bytes(long long n);
+int tvb_dot(const double* d_a, const double* d_b, const double* d_w, long long n, double* d_out, void* d_ws,
+            size_t ws_bytes, void* stream);
+
+/* a5: deflation space (DeflationSpace._build_basis, fea.py:113-183).
+ * Per block B (id = bx + mx*(by + my*bz), mx = ceil(nx/block), ...):
+ *   d_cen  f64[3*Nb]  structural centroid (grid units, relative to block corner)
+ *   d_S    f64[36*Nb] raw-mode -> orthonormal transform (0 for dropped columns)
+ *   d_keep i32[Nb]    bit j = column j kept.  Nb = mx*my*mz. */
+int tvb_defl_build(int nx, int ny, int nz, int block, double h, const double* d_occ, const uint8_t* d_nflags,
+                   double* d_cen, double* d_S, int* d_keep, void* stream);
+/* restriction yc = W^T y (6*Nb) and prolongation out = W mu / z - W mu */
+int tvb_restrict(int nx, int ny, int nz, int block, double h, const uint8_t* d_nflags, const double* d_cen,
+                 const double* d_S, const int* d_keep, const double* d_y, double* d_yc, void* stream);
+int tvb_prolong(int nx, int ny, int nz, int block, double h, const uint8_t* d_nflags, const double* d_cen,
+                const double* d_S, const int* d_keep, const double* d_mu, double* d_out, double* d_nu_ws,
+                void* stream);
+
+/* a6: Galerkin coarse operator E = W^T A W (DeflationSpace.prepare, fea.py:185-206)
+ * as a symmetrised 27-neighbour 6x6 block stencil d_Es f64[Nb*27*36];
+ * dropped/inactive coarse DOFs carry a unit diagonal.
+ * d_ws >= tvb_coarse_assemble_ws_bytes(). */
+size_t tvb_coarse_assemble_ws_bytes(int nx, int ny, int nz, int block);
+int tvb_coarse_assemble(int nx, int ny, int nz, int block, double h, const double* h_mh45, const double* d_occ,
+                        const uint8_t* d_nflags, const double* d_cen, const double* d_S, const int* d_keep,
+                        double* d_Es, void* d_ws, size_t ws_bytes, void* stream);
+/* dense (6Nb x 6Nb, row-major) copy of the block stencil (small coarse spaces) */
+int tvb_coarse_dense(int nx, int ny, int nz, int block, const double* d_Es, double* d_E, void* stream);
+
+/* a8: (deflated) Jacobi PCG -- replaces solve_static (fea.py:218-299).
+ * Synchronous: returns after convergence / the iteration cap. */
+typedef struct tvb_pcg_desc {
+  int nx, ny, nz;
+  double h;
+  const double* h_mh45;     /* 45 modal coefficients (host) */
+  const double* h_kdiag3;   /* k0[a,a], a = 0..2 (host) */
+  const double* d_occ;
+  const uint8_t* d_nflags;
+  const double* d_f;        /* right-hand side */
+  double* d_x;              /* solution (output) */
+  void* d_ws;               /* workspace, tvb_pcg_ws_bytes() */
+  size_t ws_bytes;
+  double tol;
+  int max_iters;
+  int check_every;          /* iterations per CUDA-graph launch (<= 0: default) */
+  /* deflation: block <= 0 or d_coarse == NULL -> plain Jacobi PCG */
+  int block;
+  const double* d_cen;
+  const double* d_S;
+  const int* d_keep;
+  const double* d_coarse;   /* coarse solver data (see coarse_kind) */
+  int coarse_kind;          /* 0 = dense inverse f64[nc*nc] */
+  /* outputs */
+  int iterations;
+  double residual;
+  double fnorm;
+} tvb_pcg_desc;
+
+size_t tvb_pcg_ws_bytes(int nx, int ny, int nz, int block);
+int tvb_pcg_solve(tvb_pcg_desc* desc, void* stream);
+
+/* a9/a10/a11: element state -- replaces batch_element_state (fea.py:302-309)
+ * plus the compliance sensitivity T_J and the p-norm sums
+ * (SPEC.md:292-300). Any output may be NULL. d_strains/d_stresses are
+ * f64[Ne][6] (Voigt, engineering shear), d_vm/d_tj f64[Ne];
+ * d_pn_sums (device f64[2]) <- (sum occ*vm^p, sum occ), which needs
+ * d_ws >= tvb_elem_ws_bytes(). */
+size_t tvb_elem_ws_bytes(int nx, int ny, int nz);
+int tvb_element_state(int nx, int ny, int nz, double h, double E, double nu, const double* d_u, const double* d_occ,
+                      double* d_strains, double* d_stresses, double* d_vm, double* d_tj, int p, double* d_pn_sums,
+                      void* d_ws, size_t ws_bytes, void* stream);
+/* a12: adjoint right-hand side d sigma_PN / du, fixed DOFs
+ * zeroed; d_pn_sums from tvb_element_state; d_ws >= 48*Ne bytes. */
+int tvb_adjoint_rhs(int nx, int ny, int nz, double h, double E, double nu, const double* d_u, const double* d_occ,
+                    const uint8_t* d_nflags, int p, const double* d_pn_sums, double* d_rhs, void* d_ws,
+                    size_t ws_bytes, void* stream);
+/* a13: stress sensitivity T_sigma from u and the adjoint */
+int tvb_sens_stress(int nx, int ny, int nz, double h, double E, double nu, const double* d_u, const double* d_lam,
+                    const double* d_occ, double* d_ts, void* stream);
+/* a14: max|t| and T_L = sum_i w_i t_i / max|t_i| (normalize_field + combine,
+ * SPEC.md:375-392). h_fields: host array of k device pointers. */
+int tvb_maxabs(const double* d_t, long long n, double* d_out, void* d_ws, size_t ws_bytes, void* stream);
+int tvb_combine(int k, const double* const* h_fields, const double* h_w, const double* d_maxabs, long long n,
+                double* d_out, void* stream);
+/* a15: extract: keep the k largest level-set values among
+ * design elements (ties by ascending element index) -> d_occ = 1, other
+ * design elements = ersatz, non-design = nondesign. h_state4 (optional,
+ * synchronous copy) <- {tau key, -, ties taken, #greater}. */
+size_t tvb_select_ws_bytes(long long n);
+int tvb_threshold_select(const double* d_ls, const uint8_t* d_design, long long n, long long k, double ersatz,
+                         double nondesign, double* d_occ, void* d_ws, size_t ws_bytes,
+                         unsigned long long* h_state4, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOPOVOX_B200_H */

@@ -1,0 +1,419 @@
+// extern "C" boundary of libtopovox_b200.so (declarations: include/topovox_b200.h).
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "../../include/topovox_b200.h"
+#include "deflation.cuh"
+#include "fields.cuh"
+#include "matvec.cuh"
+#include "solver.cuh"
+#include "vec.cuh"
+
+namespace tvb {
+
+static thread_local std::string g_last_error;
+void set_last_error(const char* msg) { g_last_error = msg ? msg : ""; }
+
+#include "modal_entries.inc"
+
+static int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+static int check(cudaError_t e) {
+  if (e != cudaSuccess) {
+    set_last_error(cudaGetErrorString(e));
+    return kStatusCuda;
+  }
+  return kStatusOk;
+}
+
+static bool bad_dims(int nx, int ny, int nz) { return nx < 1 || ny < 1 || nz < 1; }
+
+static Modal load_modal(const double* h) {
+  Modal m;
+  memcpy(m.mh, h, sizeof(m.mh));
+  return m;
+}
+
+__global__ void k_sum_partials(const double* partials, int n, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += partials[i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void k_subset_scale(const long long* elems, long long m, long long ne, int* counts) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const long long e = elems[i];
+  if (e >= 0 && e < ne) atomicAdd(counts + e, 1);
+}
+
+__global__ void k_subset_occ(long long ne, const int* counts, const double* occ, double* out) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= ne) return;
+  out[e] = counts[e] ? (double)counts[e] * occ[e] : 0.0;
+}
+
+}  // namespace tvb
+
+using namespace tvb;
+
+extern "C" {
+
+int tvb_version(void) { return 1; }
+
+const char* tvb_last_error(void) { return g_last_error.c_str(); }
+
+int tvb_modal_from_k0(const double* k0, double* mh45) {
+  // VTK local node -> binary index (ox + 2 oy + 4 oz)
+  static const int vtk_bin[8] = {0, 1, 3, 2, 4, 5, 7, 6};
+  double kb[24][24];
+  for (int n = 0; n < 8; ++n)
+    for (int a = 0; a < 3; ++a)
+      for (int m = 0; m < 8; ++m)
+        for (int c = 0; c < 3; ++c) kb[3 * vtk_bin[n] + a][3 * vtk_bin[m] + c] = k0[(3 * n + a) * 24 + 3 * m + c];
+  double H[8][8];
+  for (int b = 0; b < 8; ++b)
+    for (int m = 0; m < 8; ++m) {
+      double v = 1.0;
+      for (int ax = 0; ax < 3; ++ax)
+        if ((m >> ax) & 1) v *= ((b >> ax) & 1) ? 1.0 : -1.0;
+      H[b][m] = v;
+    }
+  // Mh = H3^T kb H3 / 64
+  double T[24][24], M[24][24];
+  for (int i = 0; i < 24; ++i)
+    for (int mj = 0; mj < 24; ++mj) {
+      double s = 0.0;
+      const int m = mj / 3, c = mj % 3;
+      for (int b = 0; b < 8; ++b) s += kb[i][3 * b + c] * H[b][m];
+      T[i][mj] = s;
+    }
+  double mx = 0.0;
+  for (int mi = 0; mi < 24; ++mi)
+    for (int mj = 0; mj < 24; ++mj) {
+      double s = 0.0;
+      const int m = mi / 3, a = mi % 3;
+      for (int b = 0; b < 8; ++b) s += H[b][m] * T[3 * b + a][mj];
+      M[mi][mj] = s / 64.0;
+      mx = fmax(mx, fabs(M[mi][mj]));
+    }
+  bool on[24][24] = {};
+  for (int t = 0; t < 45; ++t) {
+    on[kModalEntries[t][0]][kModalEntries[t][1]] = true;
+    mh45[t] = M[kModalEntries[t][0]][kModalEntries[t][1]];
+  }
+  for (int i = 0; i < 24; ++i)
+    for (int j = 0; j < 24; ++j)
+      if (!on[i][j] && fabs(M[i][j]) > 1e-13 * fmax(mx, 1e-300)) {
+        set_last_error("k0 is not the stiffness of an isotropic cube (mode pattern violated)");
+        return kStatusBadArg;
+      }
+  return kStatusOk;
+}
+
+size_t tvb_matvec_ws_bytes(int nx, int ny, int nz) {
+  if (bad_dims(nx, ny, nz)) return 0;
+  const MatvecPlan pl = plan_matvec(make_grid(nx, ny, nz), num_sms());
+  return sizeof(double) * ((size_t)pl.nblocks() + 1);
+}
+
+int tvb_matvec(int nx, int ny, int nz, const double* h_mh45, const double* d_u, double* d_out, const double* d_occ,
+               const uint8_t* d_nflags, int flags, double* d_dot, void* d_ws, size_t ws_bytes, void* stream) {
+  if (bad_dims(nx, ny, nz) || !h_mh45 || !d_u || !d_out || !d_occ) return kStatusBadArg;
+  if ((flags & (TVB_MASK_IN | TVB_MASK_OUT)) && !d_nflags) return kStatusBadArg;
+  const Grid g = make_grid(nx, ny, nz);
+  const MatvecPlan pl = plan_matvec(g, num_sms());
+  if (d_dot && (ws_bytes < sizeof(double) * (size_t)pl.nblocks() || !d_ws)) {
+    set_last_error("matvec workspace too small");
+    return kStatusWorkspace;
+  }
+  MatvecParams P{};
+  P.g = g;
+  P.u = d_u;
+  P.y = d_out;
+  P.occ = d_occ;
+  P.fixed = d_nflags;
+  P.mask_in = (flags & TVB_MASK_IN) ? 1 : 0;
+  P.mask_out = (flags & TVB_MASK_OUT) ? 1 : 0;
+  P.accumulate = (flags & TVB_ACCUMULATE) ? 1 : 0;
+  P.dot_partial = d_dot ? (double*)d_ws : nullptr;
+  P.stop = nullptr;
+  cudaStream_t s = (cudaStream_t)stream;
+  int st = check(launch_matvec(pl, P, load_modal(h_mh45), s));
+  if (st || !d_dot) return st;
+  k_sum_partials<<<1, 256, 0, s>>>((const double*)d_ws, pl.nblocks(), d_dot);
+  return check(cudaGetLastError());
+}
+
+int tvb_matvec_subset(int nx, int ny, int nz, const double* h_mh45, const double* d_u, double* d_out,
+                      const long long* d_elems, long long n_listed, const double* d_occ, void* d_ws, size_t ws_bytes,
+                      void* stream) {
+  if (bad_dims(nx, ny, nz) || !h_mh45 || !d_u || !d_out || !d_occ || !d_ws) return kStatusBadArg;
+  const Grid g = make_grid(nx, ny, nz);
+  const size_t need = (size_t)g.ne * (sizeof(double) + sizeof(int));
+  if (ws_bytes < need) {
+    set_last_error("subset workspace too small");
+    return kStatusWorkspace;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  double* occ_sub = (double*)d_ws;
+  int* counts = (int*)(occ_sub + g.ne);
+  if (int st = check(cudaMemsetAsync(counts, 0, g.ne * sizeof(int), s))) return st;
+  if (n_listed > 0)
+    k_subset_scale<<<(unsigned)((n_listed + 255) / 256), 256, 0, s>>>(d_elems, n_listed, g.ne, counts);
+  k_subset_occ<<<(unsigned)((g.ne + 255) / 256), 256, 0, s>>>(g.ne, counts, d_occ, occ_sub);
+  if (int st = check(cudaGetLastError())) return st;
+  return tvb_matvec(nx, ny, nz, h_mh45, d_u, d_out, occ_sub, nullptr, TVB_ACCUMULATE, nullptr, nullptr, 0, stream);
+}
+
+int tvb_diag(int nx, int ny, int nz, const double* d_occ, const uint8_t* d_nflags, const double* h_kdiag3,
+             double* d_diag, int accumulate, double* d_inv, int* d_zero_free, void* stream) {
+  if (bad_dims(nx, ny, nz) || !d_occ || !h_kdiag3) return kStatusBadArg;
+  const Grid g = make_grid(nx, ny, nz);
+  return check(launch_inv_diag(g, d_occ, d_nflags, h_kdiag3, d_inv, d_diag, d_zero_free, (cudaStream_t)stream,
+                               accumulate));
+}
+
+int tvb_node_flags(int nx, int ny, int nz, const long long* d_fixed_dofs, long long n_fixed, const double* d_occ,
+                   uint8_t* d_nflags, void* stream) {
+  if (bad_dims(nx, ny, nz) || !d_occ || !d_nflags || (n_fixed > 0 && !d_fixed_dofs)) return kStatusBadArg;
+  return check(launch_node_flags(make_grid(nx, ny, nz), d_fixed_dofs, n_fixed, d_occ, d_nflags, (cudaStream_t)stream));
+}
+
+size_t tvb_reduce_ws_bytes(long long n) { return sizeof(double) * (size_t)(reduce_grid(n) + 8); }
+
+int tvb_dot(const double* d_a, const double* d_b, const double* d_w, long long n, double* d_out, void* d_ws,
+            size_t ws_bytes, void* stream) {
+  if (!d_a || !d_b || !d_out || !d_ws || n < 0) return kStatusBadArg;
+  if (ws_bytes < tvb_reduce_ws_bytes(n)) return kStatusWorkspace;
+  double* partials = (double*)d_ws;
+  unsigned int* counter = (unsigned int*)(partials + reduce_grid(n) + 4);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int st = check(cudaMemsetAsync(counter, 0, sizeof(unsigned int), s))) return st;
+  return check(launch_dot(d_a, d_b, d_w, n, partials, counter, d_out, s));
+}
+
+int tvb_defl_build(int nx, int ny, int nz, int block, double h, const double* d_occ, const uint8_t* d_nflags,
+                   double* d_cen, double* d_S, int* d_keep, void* stream) {
+  if (bad_dims(nx, ny, nz) || block < 2 || !(h > 0.0)) return kStatusBadArg;
+  const Agglo A = make_agglo(make_grid(nx, ny, nz), block, h);
+  return check(launch_block_basis(A, d_occ, d_nflags, DeflData{d_cen, d_S, d_keep}, (cudaStream_t)stream));
+}
+
+int tvb_restrict(int nx, int ny, int nz, int block, double h, const uint8_t* d_nflags, const double* d_cen,
+                 const double* d_S, const int* d_keep, const double* d_y, double* d_yc, void* stream) {
+  if (bad_dims(nx, ny, nz) || block < 2) return kStatusBadArg;
+  const Agglo A = make_agglo(make_grid(nx, ny, nz), block, h);
+  DeflData D{const_cast<double*>(d_cen), const_cast<double*>(d_S), const_cast<int*>(d_keep)};
+  return check(launch_restrict(A, d_nflags, D, d_y, d_yc, (cudaStream_t)stream));
+}
+
+int tvb_prolong(int nx, int ny, int nz, int block, double h, const uint8_t* d_nflags, const double* d_cen,
+                const double* d_S, const int* d_keep, const double* d_mu, double* d_out, double* d_nu_ws,
+                void* stream) {
+  if (bad_dims(nx, ny, nz) || block < 2 || !d_nu_ws) return kStatusBadArg;
+  const Agglo A = make_agglo(make_grid(nx, ny, nz), block, h);
+  DeflData D{const_cast<double*>(d_cen), const_cast<double*>(d_S), const_cast<int*>(d_keep)};
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int st = check(launch_block_nu(A, D, d_mu, d_nu_ws, s))) return st;
+  return check(launch_prolong(A, d_nflags, D, d_nu_ws, d_out, nullptr, nullptr, 0, s));
+}
+
+size_t tvb_coarse_assemble_ws_bytes(int nx, int ny, int nz, int block) {
+  if (bad_dims(nx, ny, nz) || block < 2) return 0;
+  const Grid g = make_grid(nx, ny, nz);
+  const Agglo A = make_agglo(g, block, 1.0);
+  return sizeof(double) * (2 * 3 * (size_t)g.nn + 2 * 6 * (size_t)A.nb + (size_t)A.nb * 27 * 36) + 1024;
+}
+
+int tvb_coarse_assemble(int nx, int ny, int nz, int block, double h, const double* h_mh45, const double* d_occ,
+                        const uint8_t* d_nflags, const double* d_cen, const double* d_S, const int* d_keep,
+                        double* d_Es, void* d_ws, size_t ws_bytes, void* stream) {
+  if (bad_dims(nx, ny, nz) || block < 2 || !h_mh45) return kStatusBadArg;
+  if (ws_bytes < tvb_coarse_assemble_ws_bytes(nx, ny, nz, block)) return kStatusWorkspace;
+  const Grid g = make_grid(nx, ny, nz);
+  const Agglo A = make_agglo(g, block, h);
+  DeflData D{const_cast<double*>(d_cen), const_cast<double*>(d_S), const_cast<int*>(d_keep)};
+  cudaStream_t s = (cudaStream_t)stream;
+  double* v = (double*)d_ws;
+  double* t = v + 3 * g.nn;
+  double* nu = t + 3 * g.nn;
+  double* yc = nu + 6 * A.nb;
+  double* Eb = yc + 6 * A.nb;
+  const MatvecPlan pl = plan_matvec(g, num_sms());
+  const Modal M = load_modal(h_mh45);
+  if (int st = check(cudaMemsetAsync(Eb, 0, sizeof(double) * A.nb * 27 * 36, s))) return st;
+  for (int color = 0; color < 27; ++color) {
+    for (int j = 0; j < 6; ++j) {
+      if (int st = check(launch_probe_nu(A, D, color, j, nu, s))) return st;
+      if (int st = check(launch_prolong(A, d_nflags, D, nu, v, nullptr, nullptr, 0, s))) return st;
+      MatvecParams P{};
+      P.g = g;
+      P.u = v;
+      P.y = t;
+      P.occ = d_occ;
+      P.fixed = d_nflags;
+      if (int st = check(launch_matvec(pl, P, M, s))) return st;
+      if (int st = check(launch_restrict(A, d_nflags, D, t, yc, s))) return st;
+      if (int st = check(launch_probe_scatter(A, color, j, yc, Eb, s))) return st;
+    }
+  }
+  return check(launch_coarse_finish(A, D, Eb, d_Es, s));
+}
+
+int tvb_coarse_dense(int nx, int ny, int nz, int block, const double* d_Es, double* d_E, void* stream) {
+  if (bad_dims(nx, ny, nz) || block < 2) return kStatusBadArg;
+  const Agglo A = make_agglo(make_grid(nx, ny, nz), block, 1.0);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t nc = 6 * (size_t)A.nb;
+  if (int st = check(cudaMemsetAsync(d_E, 0, sizeof(double) * nc * nc, s))) return st;
+  return check(launch_coarse_dense(A, d_Es, d_E, s));
+}
+
+size_t tvb_pcg_ws_bytes(int nx, int ny, int nz, int block) {
+  if (bad_dims(nx, ny, nz)) return 0;
+  return pcg_ws_bytes(make_grid(nx, ny, nz), block);
+}
+
+int tvb_pcg_solve(tvb_pcg_desc* d, void* stream) {
+  if (!d || bad_dims(d->nx, d->ny, d->nz) || !d->h_mh45 || !d->h_kdiag3 || !d->d_occ || !d->d_nflags || !d->d_f ||
+      !d->d_x || !d->d_ws)
+    return kStatusBadArg;
+  if (!(d->tol > 0.0) || d->max_iters < 1) return kStatusBadArg;
+  PcgProblem P{};
+  P.g = make_grid(d->nx, d->ny, d->nz);
+  P.h = d->h;
+  P.modal = load_modal(d->h_mh45);
+  for (int a = 0; a < 3; ++a) P.kdiag[a] = d->h_kdiag3[a];
+  P.occ = d->d_occ;
+  P.nflags = d->d_nflags;
+  P.f = d->d_f;
+  P.x = d->d_x;
+  P.ws = d->d_ws;
+  P.ws_bytes = d->ws_bytes;
+  P.tol = d->tol;
+  P.max_iters = d->max_iters;
+  P.check_every = d->check_every;
+  P.block = (d->d_coarse != nullptr) ? d->block : 0;
+  P.cen = d->d_cen;
+  P.S = d->d_S;
+  P.keep = d->d_keep;
+  P.coarse = d->d_coarse;
+  P.coarse_kind = d->coarse_kind;
+  if (P.block > 0 && (!P.cen || !P.S || !P.keep)) return kStatusBadArg;
+  PcgResult R;
+  const int st = pcg_solve(P, R, (cudaStream_t)stream);
+  d->iterations = R.iterations;
+  d->residual = R.residual;
+  d->fnorm = R.fnorm;
+  return st;
+}
+
+static Elastic elastic(double E, double nu) {
+  const double c = E / ((1.0 + nu) * (1.0 - 2.0 * nu));
+  Elastic D;
+  D.d0 = c * (1.0 - nu);
+  D.d1 = c * nu;
+  D.d2 = c * (1.0 - 2.0 * nu) / 2.0;
+  D.c1 = 4.0 / (1.0 + nu);
+  D.c2 = (1.0 - 3.0 * nu) / (1.0 - nu * nu);
+  return D;
+}
+
+static ElemArgs elem_args(int nx, int ny, int nz, double h, double E, double nu, const double* u, const double* occ) {
+  ElemArgs A{};
+  A.g = make_grid(nx, ny, nz);
+  A.D = elastic(E, nu);
+  A.inv4h = 1.0 / (4.0 * h);
+  A.u = u;
+  A.occ = occ;
+  return A;
+}
+
+size_t tvb_elem_ws_bytes(int nx, int ny, int nz) {
+  if (bad_dims(nx, ny, nz)) return 0;
+  const long long ne = (long long)nx * ny * nz;
+  return sizeof(double) * (2 * (size_t)elem_grid(ne) + 8);
+}
+
+int tvb_element_state(int nx, int ny, int nz, double h, double E, double nu, const double* d_u, const double* d_occ,
+                      double* d_strains, double* d_stresses, double* d_vm, double* d_tj, int p, double* d_pn_sums,
+                      void* d_ws, size_t ws_bytes, void* stream) {
+  if (bad_dims(nx, ny, nz) || !d_u || !d_occ || !(h > 0.0)) return kStatusBadArg;
+  ElemArgs A = elem_args(nx, ny, nz, h, E, nu, d_u, d_occ);
+  A.strains = d_strains;
+  A.stresses = d_stresses;
+  A.vm = d_vm;
+  A.tj = d_tj;
+  A.p = p;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (d_pn_sums) {
+    if (!d_ws || ws_bytes < tvb_elem_ws_bytes(nx, ny, nz) || p < 1) return kStatusWorkspace;
+    A.pnorm_partials = (double*)d_ws;
+  }
+  if (int st = check(launch_element_state(A, s))) return st;
+  if (d_pn_sums) return check(launch_sum_pairs((const double*)d_ws, elem_grid(A.g.ne), d_pn_sums, s));
+  return kStatusOk;
+}
+
+int tvb_adjoint_rhs(int nx, int ny, int nz, double h, double E, double nu, const double* d_u, const double* d_occ,
+                    const uint8_t* d_nflags, int p, const double* d_pn_sums, double* d_rhs, void* d_ws,
+                    size_t ws_bytes, void* stream) {
+  if (bad_dims(nx, ny, nz) || !d_u || !d_occ || !d_pn_sums || !d_rhs || p < 2) return kStatusBadArg;
+  ElemArgs A = elem_args(nx, ny, nz, h, E, nu, d_u, d_occ);
+  A.p = p;
+  if (!d_ws || ws_bytes < sizeof(double) * 6 * (size_t)A.g.ne) return kStatusWorkspace;
+  return check(launch_adjoint(A, d_pn_sums, (double*)d_ws, d_nflags, d_rhs, (cudaStream_t)stream));
+}
+
+int tvb_sens_stress(int nx, int ny, int nz, double h, double E, double nu, const double* d_u, const double* d_lam,
+                    const double* d_occ, double* d_ts, void* stream) {
+  if (bad_dims(nx, ny, nz) || !d_u || !d_lam || !d_occ || !d_ts) return kStatusBadArg;
+  const ElemArgs A = elem_args(nx, ny, nz, h, E, nu, d_u, d_occ);
+  return check(launch_stress_sens(A, d_lam, d_ts, (cudaStream_t)stream));
+}
+
+int tvb_maxabs(const double* d_t, long long n, double* d_out, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!d_t || !d_out || n < 0) return kStatusBadArg;
+  if (!d_ws || ws_bytes < sizeof(double) * 1184) return kStatusWorkspace;
+  return check(launch_maxabs(d_t, n, (double*)d_ws, d_out, (cudaStream_t)stream));
+}
+
+int tvb_combine(int k, const double* const* h_fields, const double* h_w, const double* d_maxabs, long long n,
+                double* d_out, void* stream) {
+  if (k < 1 || k > kMaxFields || !h_fields || !h_w || !d_maxabs || !d_out) return kStatusBadArg;
+  CombineArgs C{};
+  C.k = k;
+  for (int i = 0; i < k; ++i) {
+    C.f[i] = h_fields[i];
+    C.w[i] = h_w[i];
+  }
+  C.maxabs = d_maxabs;
+  return check(launch_combine(C, n, d_out, (cudaStream_t)stream));
+}
+
+size_t tvb_select_ws_bytes(long long n) { return select_ws_bytes(n); }
+
+int tvb_threshold_select(const double* d_ls, const uint8_t* d_design, long long n, long long k, double ersatz,
+                         double nondesign, double* d_occ, void* d_ws, size_t ws_bytes, unsigned long long* h_state4,
+                         void* stream) {
+  if (!d_ls || !d_occ || n < 1 || k < 0 || k > n) return kStatusBadArg;
+  if (!d_ws || ws_bytes < select_ws_bytes(n)) return kStatusWorkspace;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int st = check(launch_select(d_ls, d_design, n, k, ersatz, nondesign, d_occ, d_ws, h_state4, s))) return st;
+  if (h_state4) return check(cudaStreamSynchronize(s));
+  return kStatusOk;
+}
+
+}  // extern "C"

@@ -1,0 +1,105 @@
+// Shared definitions for the sm_100a voxel-FEA kernels.
+//
+// Layout in HBM (all fp64 unless noted), reference numbering
+// (topovox/mesh.py:3-6):
+//   node vectors   f64[3*Nn]   interleaved (x,y,z) per node, node n = ix + px*(iy + py*iz)
+//   element data   f64[Ne]     occupancy, e = ix + nx*(iy + ny*iz)
+//   fixed mask     u8[Nn]      bit a set <=> DOF 3n+a is Dirichlet-fixed
+// No index table is ever read: every index is arithmetic in (nx, ny, nz).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tvb {
+
+struct Grid {
+  int nx, ny, nz;      // elements per axis
+  int px, py, pz;      // nodes per axis (= n + 1)
+  long long ne, nn;    // element / node counts
+  __host__ __device__ long long node(int x, int y, int z) const {
+    return (long long)x + (long long)px * ((long long)y + (long long)py * z);
+  }
+  __host__ __device__ long long elem(int x, int y, int z) const {
+    return (long long)x + (long long)nx * ((long long)y + (long long)ny * z);
+  }
+};
+
+inline Grid make_grid(int nx, int ny, int nz) {
+  Grid g;
+  g.nx = nx; g.ny = ny; g.nz = nz;
+  g.px = nx + 1; g.py = ny + 1; g.pz = nz + 1;
+  g.ne = (long long)nx * ny * nz;
+  g.nn = (long long)g.px * g.py * g.pz;
+  return g;
+}
+
+// The 45 mode-space coefficients of the element stiffness (gen_modal.py),
+// passed by value so they live in the kernel-parameter constant bank and feed
+// DFMA operands directly.
+struct Modal {
+  double mh[45];
+};
+
+constexpr int kStatusOk = 0;
+constexpr int kStatusBadDims = 1;
+constexpr int kStatusCuda = 2;
+constexpr int kStatusNotSpd = 3;
+constexpr int kStatusNoConvergence = 4;
+constexpr int kStatusSingular = 5;
+constexpr int kStatusBadArg = 6;
+constexpr int kStatusWorkspace = 7;
+
+// Deterministic block reduction helpers -----------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Sum over the CTA in a fixed order (warp tree, then warp 0 over warp sums).
+// Result valid in thread 0. `scratch` must hold blockDim.x/32 doubles.
+__device__ __forceinline__ double block_sum(double v, double* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (wid == 0) {
+    r = lane < nw ? scratch[lane] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;
+}
+
+__device__ __forceinline__ double block_max(double v, double* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (wid == 0) {
+    r = lane < nw ? scratch[lane] : 0.0;
+    r = warp_max(r);
+  }
+  return r;
+}
+
+// cp.async helpers (LDGSTS) ------------------------------------------------
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+}  // namespace tvb

@@ -1,0 +1,426 @@
+// K10-K14: per-element state, topological sensitivities and level-set
+// extraction.
+//
+//   k_element_state   batch_element_state (topovox/fea.py:302-309) + T_J
+//                      + p-norm partial sums
+//   k_stress_sens     T_sigma
+//   k_adjoint_h/gather  d sigma_PN / du as an atomic-free
+//                     node gather
+//   k_maxabs/k_combine  normalize_field + combine
+//   radix select      extract: order-statistic threshold with
+//                     ascending-index tie-break, exact and deterministic
+//
+// All element maps are HBM-bound streaming kernels: one thread per element,
+// the 8 corner nodes gathered from the interleaved node vector (neighbouring
+// threads share nodes through L1/L2).
+#include "fields.cuh"
+#include "vec.cuh"
+
+namespace tvb {
+
+// Centroid strain (Voigt, engineering shear) from the element's 24 DOFs:
+// B_c has entries +-1/(4h) (shape-function gradients at the centroid).
+__device__ __forceinline__ void centroid_strain(const Grid& G, const double* __restrict__ u, int ex, int ey, int ez,
+                                                double inv4h, double (&eps)[6]) {
+  double gx[3] = {0, 0, 0}, gy[3] = {0, 0, 0}, gz[3] = {0, 0, 0};  // d u_a / d x, y, z
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const int ox = b & 1, oy = (b >> 1) & 1, oz = b >> 2;
+    const long long n = G.node(ex + ox, ey + oy, ez + oz);
+    const double sx = ox ? 1.0 : -1.0, sy = oy ? 1.0 : -1.0, sz = oz ? 1.0 : -1.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double v = __ldg(u + 3 * n + a);
+      gx[a] = fma(sx, v, gx[a]);
+      gy[a] = fma(sy, v, gy[a]);
+      gz[a] = fma(sz, v, gz[a]);
+    }
+  }
+  eps[0] = gx[0] * inv4h;
+  eps[1] = gy[1] * inv4h;
+  eps[2] = gz[2] * inv4h;
+  eps[3] = (gy[0] + gx[1]) * inv4h;
+  eps[4] = (gz[1] + gy[2]) * inv4h;
+  eps[5] = (gz[0] + gx[2]) * inv4h;
+}
+
+__device__ __forceinline__ void stress_of(const Elastic& D, double occ, const double (&e)[6], double (&s)[6]) {
+  const double tr = e[0] + e[1] + e[2];
+  s[0] = occ * fma(D.d0 - D.d1, e[0], D.d1 * tr);
+  s[1] = occ * fma(D.d0 - D.d1, e[1], D.d1 * tr);
+  s[2] = occ * fma(D.d0 - D.d1, e[2], D.d1 * tr);
+  s[3] = occ * (D.d2 * e[3]);
+  s[4] = occ * (D.d2 * e[4]);
+  s[5] = occ * (D.d2 * e[5]);
+}
+
+__device__ __forceinline__ double vm_of(const double (&s)[6]) {
+  const double q = s[0] * s[0] + s[1] * s[1] + s[2] * s[2] - s[0] * s[1] - s[1] * s[2] - s[0] * s[2] +
+                   3.0 * (s[3] * s[3] + s[4] * s[4] + s[5] * s[5]);
+  return sqrt(fmax(q, 0.0));
+}
+
+// 4/(1+nu) s.e - (1-3nu)/(1-nu^2) tr(s) tr(e)
+__device__ __forceinline__ double sens_of(const Elastic& D, const double (&s)[6], const double (&e)[6]) {
+  double se = 0.0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) se = fma(s[i], e[i], se);
+  const double trs = s[0] + s[1] + s[2], tre = e[0] + e[1] + e[2];
+  return D.c1 * se - D.c2 * trs * tre;
+}
+
+__device__ __forceinline__ void elem_xyz(const Grid& G, long long e, int& ex, int& ey, int& ez) {
+  ex = (int)(e % G.nx);
+  ey = (int)((e / G.nx) % G.ny);
+  ez = (int)(e / ((long long)G.nx * G.ny));
+}
+
+// powi for the (even, small) p-norm exponent; exact repeated squaring
+__device__ __forceinline__ double powi(double x, int p) {
+  double r = 1.0;
+  double b = x;
+  while (p > 0) {
+    if (p & 1) r *= b;
+    b *= b;
+    p >>= 1;
+  }
+  return r;
+}
+
+__global__ void k_element_state(ElemArgs A) {
+  __shared__ double red[32];
+  const Grid& G = A.g;
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  double pn = 0.0, oc = 0.0;
+  if (e < G.ne) {
+    int ex, ey, ez;
+    elem_xyz(G, e, ex, ey, ez);
+    double eps[6], sig[6];
+    centroid_strain(G, A.u, ex, ey, ez, A.inv4h, eps);
+    const double occ = A.occ[e];
+    stress_of(A.D, occ, eps, sig);
+    const double vm = vm_of(sig);
+    if (A.strains)
+      for (int i = 0; i < 6; ++i) A.strains[6 * e + i] = eps[i];
+    if (A.stresses)
+      for (int i = 0; i < 6; ++i) A.stresses[6 * e + i] = sig[i];
+    if (A.vm) A.vm[e] = vm;
+    if (A.tj) A.tj[e] = sens_of(A.D, sig, eps);
+    if (A.pnorm_partials) {
+      pn = occ * powi(vm, A.p);
+      oc = occ;
+    }
+  }
+  if (A.pnorm_partials) {
+    pn = block_sum(pn, red);
+    oc = block_sum(oc, red);
+    if (threadIdx.x == 0) {
+      A.pnorm_partials[2 * blockIdx.x] = pn;
+      A.pnorm_partials[2 * blockIdx.x + 1] = oc;
+    }
+  }
+}
+
+__global__ void k_stress_sens(ElemArgs A, const double* lam, double* ts) {
+  const Grid& G = A.g;
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= G.ne) return;
+  int ex, ey, ez;
+  elem_xyz(G, e, ex, ey, ez);
+  double eu[6], sig[6], el[6];
+  centroid_strain(G, A.u, ex, ey, ez, A.inv4h, eu);
+  stress_of(A.D, A.occ[e], eu, sig);
+  centroid_strain(G, lam, ex, ey, ez, A.inv4h, el);
+  ts[e] = sens_of(A.D, sig, el);
+}
+
+// h_e = S^(1/p-1) w_e vm^(p-2) occ_e * D Q sigma_e   (w_e = occ_e / sum occ)
+__global__ void k_adjoint_h(ElemArgs A, const double* sums, double* h6) {
+  const Grid& G = A.g;
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= G.ne) return;
+  const double S = sums[0] / sums[1];  // sum w vm^p with w = occ / sum(occ)
+  const double inv_occ_sum = 1.0 / sums[1];
+  int ex, ey, ez;
+  elem_xyz(G, e, ex, ey, ez);
+  double eps[6], sig[6];
+  centroid_strain(G, A.u, ex, ey, ez, A.inv4h, eps);
+  const double occ = A.occ[e];
+  stress_of(A.D, occ, eps, sig);
+  const double vm = vm_of(sig);
+  const double coef = pow(S, 1.0 / A.p - 1.0) * (occ * inv_occ_sum) * powi(vm, A.p - 2) * occ;
+  // Q sigma
+  double qs[6];
+  qs[0] = sig[0] - 0.5 * (sig[1] + sig[2]);
+  qs[1] = sig[1] - 0.5 * (sig[0] + sig[2]);
+  qs[2] = sig[2] - 0.5 * (sig[0] + sig[1]);
+  qs[3] = 3.0 * sig[3];
+  qs[4] = 3.0 * sig[4];
+  qs[5] = 3.0 * sig[5];
+  double out[6];
+  stress_of(A.D, coef, qs, out);  // D (Q sigma) scaled
+  for (int i = 0; i < 6; ++i) h6[6 * e + i] = out[i];
+}
+
+// rhs_n = sum_{e ∋ n} B_c[:, dofs(n in e)]^T h_e, fixed DOFs zeroed. Fixed order.
+__global__ void k_adjoint_gather(Grid G, double inv4h, const double* h6, const uint8_t* nflags, double* rhs) {
+  const long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (n >= G.nn) return;
+  const int x = (int)(n % G.px), y = (int)((n / G.px) % G.py), z = (int)(n / ((long long)G.px * G.py));
+  double r[3] = {0, 0, 0};
+  for (int dz = -1; dz <= 0; ++dz)
+    for (int dy = -1; dy <= 0; ++dy)
+      for (int dx = -1; dx <= 0; ++dx) {
+        const int ex = x + dx, ey = y + dy, ez = z + dz;
+        if (ex < 0 || ex >= G.nx || ey < 0 || ey >= G.ny || ez < 0 || ez >= G.nz) continue;
+        const double* h = h6 + 6 * G.elem(ex, ey, ez);
+        // node is local corner (ox,oy,oz) = (-dx,-dy,-dz); corner sign 2*o-1
+        const double sx = dx ? 1.0 : -1.0, sy = dy ? 1.0 : -1.0, sz = dz ? 1.0 : -1.0;
+        r[0] += (sx * h[0] + sy * h[3] + sz * h[5]) * inv4h;
+        r[1] += (sy * h[1] + sx * h[3] + sz * h[4]) * inv4h;
+        r[2] += (sz * h[2] + sy * h[4] + sx * h[5]) * inv4h;
+      }
+  const uint8_t fl = nflags ? nflags[n] : 0;
+  for (int a = 0; a < 3; ++a) rhs[3 * n + a] = ((fl >> a) & 1) ? 0.0 : r[a];
+}
+
+// ---------------------------------------------------------------------------
+// max |t| (deterministic: max is order independent) and combination
+// ---------------------------------------------------------------------------
+__global__ void k_maxabs(const double* t, long long n, double* partials) {
+  __shared__ double red[32];
+  double m = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(t[i]));
+  m = block_max(m, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = m;
+}
+
+__global__ void k_maxabs_final(const double* partials, int np, double* out) {
+  __shared__ double red[32];
+  double m = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) m = fmax(m, partials[i]);
+  m = block_max(m, red);
+  if (threadIdx.x == 0) *out = m;
+}
+
+// out = sum_i w_i * t_i / max_i   (fields with weight 0 or max 0 skipped)
+__global__ void k_combine(CombineArgs C, long long n, double* out) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double v = 0.0;
+  for (int i = 0; i < C.k; ++i) {
+    const double m = C.maxabs[i];
+    if (C.w[i] == 0.0) continue;
+    const double t = (m == 0.0) ? C.f[i][e] : C.f[i][e] / m;
+    v = fma(C.w[i], t, v);
+  }
+  out[e] = v;
+}
+
+// ---------------------------------------------------------------------------
+// exact order-statistic selection (radix select on order-preserving keys)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long okey(double v) {
+  if (v == 0.0) v = 0.0;  // -0 -> +0
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// state: [0] prefix key bits, [1] prefix mask, [2] k remaining, [3] count greater
+__global__ void k_radix_hist(const double* ls, const uint8_t* design, long long n, const unsigned long long* state,
+                             int shift, unsigned int* hist) {
+  __shared__ unsigned int sh[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const unsigned long long pref = state[0], mask = state[1];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    if (design && !design[i]) continue;
+    const unsigned long long k = okey(ls[i]);
+    if ((k & mask) != pref) continue;
+    atomicAdd(&sh[(k >> shift) & 255], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// choose the digit holding the k-th largest (descending), update state, clear hist
+__global__ void k_radix_pick(unsigned long long* state, int shift, unsigned int* hist) {
+  if (threadIdx.x != 0) return;
+  unsigned long long kr = state[2];
+  unsigned long long gt = state[3];
+  int d = 255;
+  for (; d >= 0; --d) {
+    const unsigned long long c = hist[d];
+    if (c >= kr) break;
+    kr -= c;
+    gt += c;
+  }
+  if (d < 0) d = 0;
+  state[0] |= ((unsigned long long)d) << shift;
+  state[1] |= 255ull << shift;
+  state[2] = kr;
+  state[3] = gt;
+  for (int i = 0; i < 256; ++i) hist[i] = 0;
+}
+
+// per-block count of design elements whose key equals the threshold key
+__global__ void k_eq_count(const double* ls, const uint8_t* design, long long n, const unsigned long long* state,
+                           unsigned int* bcount) {
+  __shared__ unsigned int c;
+  if (threadIdx.x == 0) c = 0;
+  __syncthreads();
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n && (!design || design[i]) && okey(ls[i]) == state[0]) atomicAdd(&c, 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) bcount[blockIdx.x] = c;
+}
+
+// exclusive scan of the block counts (single CTA, sequential chunks)
+__global__ void k_scan_counts(unsigned int* bcount, int nb) {
+  __shared__ unsigned int carry;
+  __shared__ unsigned int tmp[1024];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nb; base += 1024) {
+    const int i = base + threadIdx.x;
+    const unsigned int v = i < nb ? bcount[i] : 0u;
+    tmp[threadIdx.x] = v;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+      const unsigned int a = threadIdx.x >= off ? tmp[threadIdx.x - off] : 0u;
+      __syncthreads();
+      tmp[threadIdx.x] += a;
+      __syncthreads();
+    }
+    if (i < nb) bcount[i] = carry + tmp[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += tmp[1023];
+    __syncthreads();
+  }
+}
+
+// occ = 1 for key > tau, or key == tau among the first (k - #greater) by index
+__global__ void k_apply_threshold(const double* ls, const uint8_t* design, long long n,
+                                  const unsigned long long* state, const unsigned int* boff, double ersatz,
+                                  double nondesign, double* occ) {
+  __shared__ unsigned int flags[1024];
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool in = i < n;
+  const bool des = in && (!design || design[i]);
+  const unsigned long long k = in ? okey(ls[i]) : 0ull;
+  const unsigned long long tau = state[0];
+  const bool eq = des && k == tau;
+  flags[threadIdx.x] = eq ? 1u : 0u;
+  __syncthreads();
+  for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+    const unsigned int a = threadIdx.x >= off ? flags[threadIdx.x - off] : 0u;
+    __syncthreads();
+    flags[threadIdx.x] += a;
+    __syncthreads();
+  }
+  if (!in) return;
+  const unsigned long long need = state[2];  // how many ties to take
+  const unsigned long long rank = boff[blockIdx.x] + flags[threadIdx.x] - (eq ? 1u : 0u);
+  double v;
+  if (!des) v = nondesign;
+  else if (k > tau || (eq && rank < need)) v = 1.0;
+  else v = ersatz;
+  occ[i] = v;
+}
+
+// ---------------------------------------------------------------------------
+int elem_grid(long long n) { return (int)((n + 255) / 256); }
+
+cudaError_t launch_element_state(const ElemArgs& A, cudaStream_t s) {
+  k_element_state<<<elem_grid(A.g.ne), 256, 0, s>>>(A);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stress_sens(const ElemArgs& A, const double* lam, double* ts, cudaStream_t s) {
+  k_stress_sens<<<elem_grid(A.g.ne), 256, 0, s>>>(A, lam, ts);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_adjoint(const ElemArgs& A, const double* sums, double* h6, const uint8_t* nflags, double* rhs,
+                           cudaStream_t s) {
+  k_adjoint_h<<<elem_grid(A.g.ne), 256, 0, s>>>(A, sums, h6);
+  k_adjoint_gather<<<(unsigned)((A.g.nn + 255) / 256), 256, 0, s>>>(A.g, A.inv4h, h6, nflags, rhs);
+  return cudaGetLastError();
+}
+
+__global__ void k_sum_pairs(const double* partials, int np, double* out) {
+  __shared__ double red[32];
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    a += partials[2 * i];
+    b += partials[2 * i + 1];
+  }
+  a = block_sum(a, red);
+  b = block_sum(b, red);
+  if (threadIdx.x == 0) {
+    out[0] = a;
+    out[1] = b;
+  }
+}
+
+cudaError_t launch_sum_pairs(const double* partials, int np, double* out2, cudaStream_t s) {
+  k_sum_pairs<<<1, 256, 0, s>>>(partials, np, out2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_maxabs(const double* t, long long n, double* partials, double* out, cudaStream_t s) {
+  int nb = (int)((n + 255) / 256);
+  if (nb > 1184) nb = 1184;
+  if (nb < 1) nb = 1;
+  k_maxabs<<<nb, 256, 0, s>>>(t, n, partials);
+  k_maxabs_final<<<1, 256, 0, s>>>(partials, nb, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine(const CombineArgs& C, long long n, double* out, cudaStream_t s) {
+  k_combine<<<elem_grid(n), 256, 0, s>>>(C, n, out);
+  return cudaGetLastError();
+}
+
+size_t select_ws_bytes(long long n) {
+  const long long nb = (n + 1023) / 1024;
+  return 64 + 256 * sizeof(unsigned int) + (size_t)nb * sizeof(unsigned int) + 64;
+}
+
+cudaError_t launch_select(const double* ls, const uint8_t* design, long long n, long long k, double ersatz,
+                          double nondesign, double* occ, void* ws, unsigned long long* state_out, cudaStream_t s) {
+  unsigned long long* state = (unsigned long long*)ws;
+  unsigned int* hist = (unsigned int*)((char*)ws + 64);
+  unsigned int* bcount = hist + 256;
+  const unsigned long long init[4] = {0ull, 0ull, (unsigned long long)(k > 0 ? k : 1), 0ull};
+  cudaError_t e = cudaMemcpyAsync(state, init, sizeof(init), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(hist, 0, 256 * sizeof(unsigned int), s);
+  if (e != cudaSuccess) return e;
+  int nbh = (int)((n + 255) / 256);
+  if (nbh > 1184) nbh = 1184;
+  if (nbh < 1) nbh = 1;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    k_radix_hist<<<nbh, 256, 0, s>>>(ls, design, n, state, shift, hist);
+    k_radix_pick<<<1, 32, 0, s>>>(state, shift, hist);
+  }
+  const int nb = (int)((n + 1023) / 1024);
+  if (k <= 0) {
+    // nothing retained: threshold above every key
+    const unsigned long long none[4] = {~0ull, ~0ull, 0ull, 0ull};
+    e = cudaMemcpyAsync(state, none, sizeof(none), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+  }
+  k_eq_count<<<nb, 1024, 0, s>>>(ls, design, n, state, bcount);
+  k_scan_counts<<<1, 1024, 0, s>>>(bcount, nb);
+  k_apply_threshold<<<nb, 1024, 0, s>>>(ls, design, n, state, bcount, ersatz, nondesign, occ);
+  if (state_out) {
+    e = cudaMemcpyAsync(state_out, state, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace tvb

@@ -1,0 +1,41 @@
+#pragma once
+#include "common.cuh"
+
+namespace tvb {
+
+void set_last_error(const char* msg);
+
+struct PcgProblem {
+  Grid g;
+  double h;
+  Modal modal;
+  double kdiag[3];
+  const double* occ;
+  const uint8_t* nflags;
+  const double* f;
+  double* x;
+  void* ws;
+  size_t ws_bytes;
+  double tol;
+  int max_iters;
+  int check_every;
+  int block;  // <= 0: no deflation
+  const double* cen;
+  const double* S;
+  const int* keep;
+  const double* coarse;  // dense inverse (coarse_kind 0)
+  int coarse_kind;
+};
+
+struct PcgResult {
+  int iterations = 0;
+  double residual = 0.0;
+  double fnorm = 0.0;
+};
+
+size_t pcg_ws_bytes(const Grid& g, int block);
+int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream);
+cudaError_t launch_dense_gemv(long long nc, const double* Einv, const double* yc, double* mu, const int* stop,
+                              cudaStream_t s);
+
+}  // namespace tvb
