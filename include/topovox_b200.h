@@ -59,6 +59,10 @@ int tvb_matvec(int nx, int ny, int nz, const double* h_mh45, const double* d_u, 
                const double* d_occ, const uint8_t* d_nflags, int flags, double* d_dot, void* d_ws,
                size_t ws_bytes, void* stream);
 
+/* diagnostics: the launch plan tvb_matvec uses for this grid:
+ * out7 = {threads, wx, wy, tiles_x, tiles_y, persistent CTAs, 0} */
+int tvb_matvec_plan(int nx, int ny, int nz, int* h_out7);
+
 /* apply_block24_subset (numba_kernels.py:31-46): out += K_subset u using only
  * the listed elements (duplicates count with multiplicity). d_ws: f64[Ne] + i32[Ne]. */
 int tvb_matvec_subset(int nx, int ny, int nz, const double* h_mh45, const double* d_u, double* d_out,

@@ -37,10 +37,35 @@ static int check(cudaError_t e) {
 
 static bool bad_dims(int nx, int ny, int nz) { return nx < 1 || ny < 1 || nz < 1; }
 
-static Modal load_modal(const double* h) {
-  Modal m;
-  memcpy(m.mh, h, sizeof(m.mh));
-  return m;
+// Reduce the 45 mode-space entries (kModalEntries order) to the 8 structural
+// constants of modal_apply8; false if the entries do not have the cube
+// structure (then the caller's k0 was not an isotropic cube stiffness).
+static bool modal_reduce(const double* mh, Modal& m) {
+  // representative entries: (3,3) (3,7) (4,4) (9,9) (9,20) (11,11) (11,16) (21,21)
+  static const int rep[8] = {0, 1, 3, 14, 15, 18, 19, 42};
+  static const int cls[45] = {0, 1, 1, 2, 2, 2, 2, 2, 2, 1, 0, 1, 2, 2, 3, 4, 3, 4, 5, 6, 6, 2, 2,
+                              2, 2, 1, 1, 0, 3, 4, 6, 5, 6, 4, 3, 6, 6, 5, 4, 3, 4, 3, 7, 7, 7};
+  double v[8], mx = 0.0;
+  for (int i = 0; i < 8; ++i) v[i] = mh[rep[i]];
+  for (int t = 0; t < 45; ++t) mx = fmax(mx, fabs(mh[t]));
+  for (int t = 0; t < 45; ++t)
+    if (fabs(mh[t] - v[cls[t]]) > 1e-12 * mx) return false;
+  m.k[0] = v[0] - v[1];
+  m.k[1] = v[1];
+  m.k[2] = v[2];
+  m.k[3] = v[3];
+  m.k[4] = v[4];
+  m.k[5] = v[5] - v[6];
+  m.k[6] = v[6];
+  m.k[7] = v[7];
+  return true;
+}
+
+
+__global__ void k_masked_copy(long long nn, const double* u, const uint8_t* nflags, double* out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= 3 * nn) return;
+  out[i] = ((nflags[i / 3] >> (i % 3)) & 1) ? 0.0 : u[i];
 }
 
 __global__ void k_sum_partials(const double* partials, int n, double* out) {
@@ -119,13 +144,20 @@ int tvb_modal_from_k0(const double* k0, double* mh45) {
         set_last_error("k0 is not the stiffness of an isotropic cube (mode pattern violated)");
         return kStatusBadArg;
       }
+  Modal probe;
+  if (!modal_reduce(mh45, probe)) {
+    set_last_error("k0 is not the stiffness of an isotropic cube (mode values violate the cube symmetry)");
+    return kStatusBadArg;
+  }
   return kStatusOk;
 }
 
+// workspace: per-CTA dot partials (65536 max) + a masked copy of u (MASK_IN)
+static size_t matvec_partials_bytes() { return sizeof(double) * 65536; }
+
 size_t tvb_matvec_ws_bytes(int nx, int ny, int nz) {
   if (bad_dims(nx, ny, nz)) return 0;
-  const MatvecPlan pl = plan_matvec(make_grid(nx, ny, nz), num_sms());
-  return sizeof(double) * ((size_t)pl.nblocks() + 1);
+  return matvec_partials_bytes() + sizeof(double) * 3 * (size_t)make_grid(nx, ny, nz).nn;
 }
 
 int tvb_matvec(int nx, int ny, int nz, const double* h_mh45, const double* d_u, double* d_out, const double* d_occ,
@@ -134,26 +166,43 @@ int tvb_matvec(int nx, int ny, int nz, const double* h_mh45, const double* d_u, 
   if ((flags & (TVB_MASK_IN | TVB_MASK_OUT)) && !d_nflags) return kStatusBadArg;
   const Grid g = make_grid(nx, ny, nz);
   const MatvecPlan pl = plan_matvec(g, num_sms());
-  if (d_dot && (ws_bytes < sizeof(double) * (size_t)pl.nblocks() || !d_ws)) {
+  const bool mask_in = (flags & TVB_MASK_IN) != 0;
+  if ((d_dot || mask_in) && (!d_ws || ws_bytes < tvb_matvec_ws_bytes(nx, ny, nz) || pl.nblocks() > 65536)) {
     set_last_error("matvec workspace too small");
     return kStatusWorkspace;
   }
+  Modal M;
+  if (!modal_reduce(h_mh45, M)) return kStatusBadArg;
+  cudaStream_t s = (cudaStream_t)stream;
+  const double* u = d_u;
+  if (mask_in) {
+    double* um = (double*)((char*)d_ws + matvec_partials_bytes());
+    k_masked_copy<<<(unsigned)((3 * g.nn + 255) / 256), 256, 0, s>>>(g.nn, d_u, d_nflags, um);
+    u = um;
+  }
   MatvecParams P{};
   P.g = g;
-  P.u = d_u;
+  P.u = u;
   P.y = d_out;
   P.occ = d_occ;
   P.fixed = d_nflags;
-  P.mask_in = (flags & TVB_MASK_IN) ? 1 : 0;
+  P.mask_in = 0;
   P.mask_out = (flags & TVB_MASK_OUT) ? 1 : 0;
   P.accumulate = (flags & TVB_ACCUMULATE) ? 1 : 0;
   P.dot_partial = d_dot ? (double*)d_ws : nullptr;
   P.stop = nullptr;
-  cudaStream_t s = (cudaStream_t)stream;
-  int st = check(launch_matvec(pl, P, load_modal(h_mh45), s));
+  int st = check(launch_matvec(pl, P, M, s));
   if (st || !d_dot) return st;
   k_sum_partials<<<1, 256, 0, s>>>((const double*)d_ws, pl.nblocks(), d_dot);
   return check(cudaGetLastError());
+}
+
+int tvb_matvec_plan(int nx, int ny, int nz, int* out7) {
+  if (bad_dims(nx, ny, nz) || !out7) return kStatusBadArg;
+  const MatvecPlan pl = plan_matvec(make_grid(nx, ny, nz), num_sms());
+  const int v[7] = {pl.nt, pl.wx, pl.wy, pl.ntx, pl.nty, pl.nctas, 0};
+  for (int i = 0; i < 7; ++i) out7[i] = v[i];
+  return kStatusOk;
 }
 
 int tvb_matvec_subset(int nx, int ny, int nz, const double* h_mh45, const double* d_u, double* d_out,
@@ -252,7 +301,8 @@ int tvb_coarse_assemble(int nx, int ny, int nz, int block, double h, const doubl
   double* yc = nu + 6 * A.nb;
   double* Eb = yc + 6 * A.nb;
   const MatvecPlan pl = plan_matvec(g, num_sms());
-  const Modal M = load_modal(h_mh45);
+  Modal M;
+  if (!modal_reduce(h_mh45, M)) return kStatusBadArg;
   if (int st = check(cudaMemsetAsync(Eb, 0, sizeof(double) * A.nb * 27 * 36, s))) return st;
   for (int color = 0; color < 27; ++color) {
     for (int j = 0; j < 6; ++j) {
@@ -294,7 +344,7 @@ int tvb_pcg_solve(tvb_pcg_desc* d, void* stream) {
   PcgProblem P{};
   P.g = make_grid(d->nx, d->ny, d->nz);
   P.h = d->h;
-  P.modal = load_modal(d->h_mh45);
+  if (!modal_reduce(d->h_mh45, P.modal)) return kStatusBadArg;
   for (int a = 0; a < 3; ++a) P.kdiag[a] = d->h_kdiag3[a];
   P.occ = d->d_occ;
   P.nflags = d->d_nflags;

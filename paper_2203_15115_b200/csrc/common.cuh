@@ -33,11 +33,12 @@ inline Grid make_grid(int nx, int ny, int nz) {
   return g;
 }
 
-// The 45 mode-space coefficients of the element stiffness (gen_modal.py),
-// passed by value so they live in the kernel-parameter constant bank and feed
-// DFMA operands directly.
+// The element stiffness in mode space reduced to its 8 structurally distinct
+// constants {k0-k1, k1, k2, k3, k4, k5-k6, k6, k7} (see modal_apply8 and
+// modal_reduce in capi.cu). sm_100 DFMA cannot read the constant bank, so
+// these 8 doubles are held in registers for the whole kernel.
 struct Modal {
-  double mh[45];
+  double k[8];
 };
 
 constexpr int kStatusOk = 0;
@@ -101,5 +102,9 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
 
 }  // namespace tvb

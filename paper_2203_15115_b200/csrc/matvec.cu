@@ -1,4 +1,4 @@
-// K1: assembly-free hex stiffness matvec  y = M_out * sum_e occ_e P_e^T k0 P_e * M_in u
+// K1: assembly-free hex stiffness matvec  y = M_out * sum_e occ_e P_e^T k0 P_e * u
 //
 // Replaces the numba kernel apply_block24 (topovox/backends/numba_kernels.py:12-28)
 // called from StiffnessOperator.apply (topovox/fea.py:49-65).
@@ -10,234 +10,382 @@
 //    Every output node is written by exactly one thread, which sums its 8
 //    element contributions in a fixed order: the result is bitwise
 //    deterministic and needs no atomics.
-//  * u is staged plane by plane into a 3-deep shared-memory ring with cp.async,
-//    one plane ahead of the compute.
-//  * k0 is applied in the Walsh-Hadamard mode basis of the cube (45 nonzeros
-//    instead of 576, gen_modal.py), as H3 * Mh * H3^T with butterflies.
-//  * the z-direction node sum is done in mode space in registers (the "carry"
-//    of the upper face), the x/y sums through one shared-memory exchange.
+//  * node planes of u and occupancy layers are staged into shared-memory rings
+//    with cp.async, kAhead planes ahead of the compute (enough bytes in flight
+//    per SM to cover DRAM latency); one __syncthreads per z-step.
+//  * k0 is applied in the Walsh-Hadamard mode basis of the cube: butterflies
+//    H3^T, a 33-flop mode-space operator (8 structural constants), butterflies
+//    H3 -- ~150 fp64 ops per element instead of 576 FMAs.
+//  * the bottom face's xy-transform is reused from the previous step and the
+//    z-direction node sum is done in mode space in registers ("carry"); the
+//    x/y node sums go through one double-buffered shared-memory exchange.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
 #include "matvec.cuh"
 
 namespace tvb {
 
-__device__ __forceinline__ void modal_apply(const double* __restrict__ mh, const double (&c)[24], double (&g)[24]) {
-#include "modal_apply.inc"
+// Element operator in the Walsh-Hadamard mode basis (binary local numbering,
+// modal DOF 3*mode + axis). The 45 nonzeros of Mh (gen_modal.py) take only 8
+// structurally distinct values (cube symmetry, any E, nu, h); with
+// s = occ * {k0-k1, k1, k2, k3, k4, k5-k6, k6, k7} the product is 33 flops:
+//   {3,7,14} and {11,16,18}: diagonal + rank-one coupling,
+//   {4,6} {5,12} {8,13}: all four entries equal (shear pairs),
+//   {9,20} {10,17} {15,19}: symmetric 2x2, {21},{22},{23}: diagonal.
+__device__ __forceinline__ void modal_apply8(const double (&s)[8], const double (&c)[24], double (&g)[24]) {
+  g[0] = g[1] = g[2] = 0.0;
+  const double tA = s[1] * ((c[3] + c[7]) + c[14]);
+  g[3] = fma(s[0], c[3], tA);
+  g[7] = fma(s[0], c[7], tA);
+  g[14] = fma(s[0], c[14], tA);
+  g[4] = g[6] = s[2] * (c[4] + c[6]);
+  g[5] = g[12] = s[2] * (c[5] + c[12]);
+  g[8] = g[13] = s[2] * (c[8] + c[13]);
+  g[9] = fma(s[3], c[9], s[4] * c[20]);
+  g[20] = fma(s[3], c[20], s[4] * c[9]);
+  g[10] = fma(s[3], c[10], s[4] * c[17]);
+  g[17] = fma(s[3], c[17], s[4] * c[10]);
+  g[15] = fma(s[3], c[15], s[4] * c[19]);
+  g[19] = fma(s[3], c[19], s[4] * c[15]);
+  const double tB = s[6] * ((c[11] + c[16]) + c[18]);
+  g[11] = fma(s[5], c[11], tB);
+  g[16] = fma(s[5], c[16], tB);
+  g[18] = fma(s[5], c[18], tB);
+  g[21] = s[7] * c[21];
+  g[22] = s[7] * c[22];
+  g[23] = s[7] * c[23];
 }
 
-template <int NT>
-__global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) k_matvec(MatvecParams P, Modal M) {
+// smem row stride (doubles) of a staged node plane: 3*wx + 16 makes the
+// element-column gather conflict-free even where a warp wraps to the next
+// tile row (stride == 3*wx mod 16 in 8-byte words).
+__host__ __device__ inline int plane_row_stride(int wx) { return 3 * wx + 16; }
+
+__device__ __forceinline__ void xy_forward(double (&f)[12]) {
+  // face node (ox,oy) -> face mode (mx,my); per bit: (v0,v1) -> (v0+v1, v1-v0)
+#pragma unroll
+  for (int bit = 1; bit < 4; bit <<= 1)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      if (b & bit) continue;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double v0 = f[3 * b + a], v1 = f[3 * (b | bit) + a];
+        f[3 * b + a] = v0 + v1;
+        f[3 * (b | bit) + a] = v1 - v0;
+      }
+    }
+}
+
+__device__ __forceinline__ void xy_inverse(double (&f)[12]) {
+  // face mode -> face node; per bit: (g0,g1) -> (g0-g1, g0+g1)
+#pragma unroll
+  for (int bit = 1; bit < 4; bit <<= 1)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      if (b & bit) continue;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double g0 = f[3 * b + a], g1 = f[3 * (b | bit) + a];
+        f[3 * b + a] = g0 - g1;
+        f[3 * (b | bit) + a] = g0 + g1;
+      }
+    }
+}
+
+constexpr int kXcPad = 64;  // exchange rows past NT read (harmlessly) by edge threads
+constexpr int kAhead = 4;   // node planes in flight ahead of the compute (cp.async groups)
+constexpr int kRing = kAhead + 1;
+
+// One CTA = a (wx-1) x (wy-1) column of owned nodes over z-planes [kz0, kz1).
+// Step k (element layer k between node planes k and k+1), per thread:
+//   gather the 4 top-face nodes of its element column from staged plane k+1,
+//   xy-transform them (the bottom face's transform is kept from step k-1),
+//   apply the element operator in mode space, z-accumulate the node sums of
+//   plane k in mode space (carry), and exchange the 3 non-owned face nodes of
+//   plane k through shared memory; the owner thread finishes the node.
+template <int NT, int MINB, bool DOT, bool MASKOUT>
+__global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
   extern __shared__ double smem[];
   if (P.stop != nullptr && *P.stop) return;
   const Grid& G = P.g;
   const int wx = P.wx, wy = P.wy;
-  const int PW = wx + 1, PH = wy + 1, PN = PW * PH;  // node tile of one plane
-  const int tile = blockIdx.x;
-  const int x0 = (tile % P.ntx) * (wx - 1);
-  const int y0 = (tile / P.ntx) * (wy - 1);
-  const int kz0 = blockIdx.y * P.zc;
-  const int kz1 = min(kz0 + P.zc, G.pz);  // owned planes [kz0, kz1)
+  const int PW = wx + 1, PH = wy + 1;
+  const int S = plane_row_stride(wx);
+  const int PS = PH * S;   // doubles per staged node plane
+  const int OS = wx * wy;  // doubles per staged occupancy layer
+  const long long plane_stride = 3LL * G.px * G.py;
+  const long long layer_stride = (long long)G.nx * G.ny;
 
-  double* Up = smem;                 // [3][PN*3] plane ring
-  double* Xc = smem + 9 * PN;        // [NT][9] face-node exchange
-  double* red = Xc + 9 * NT;         // [NT/32] reduction scratch
+  double* Up = smem;                  // [kRing][PS] node plane ring
+  double* Oc = Up + kRing * PS;       // [kRing][OS] occupancy layer ring
+  double* Xc = Oc + kRing * OS;       // [2][NT + kXcPad][9] face exchange
+  const int XS = 9 * (NT + kXcPad);
+  double* red = Xc + 2 * XS;
 
   const int t = threadIdx.x;
+  const int lane = t & 31, warp = t >> 5;
   const bool active = t < wx * wy;
   const int tx = active ? t % wx : 0, ty = active ? t / wx : 0;
-  const int ex = x0 - 1 + tx, ey = y0 - 1 + ty;
-  const bool col_in = active && ex >= 0 && ex < G.nx && ey >= 0 && ey < G.ny;
-  const bool owner = active && tx < wx - 1 && ty < wy - 1 && (x0 + tx) < G.px && (y0 + ty) < G.py;
-
-  auto load_plane = [&](int k) {
-    double* dst = Up + ((k + 3) % 3) * (3 * PN);
-    const bool kin = (k >= 0 && k < G.pz);
-    const int rowlen = 3 * PW;
-    for (int idx = t; idx < 3 * PN; idx += NT) {
-      const int jy = idx / rowlen, r = idx - jy * rowlen;
-      const int gx = x0 - 1 + r / 3, gy = y0 - 1 + jy;
-      if (kin && gx >= 0 && gx < G.px && gy >= 0 && gy < G.py) {
-        const long long off = 3 * G.node(x0 - 1, gy, k) + r;
-        cp_async8(dst + idx, P.u + off);
-      } else {
-        dst[idx] = 0.0;
-      }
-    }
-    cp_async_commit();
-  };
-  auto mask_plane = [&](int k) {
-    if (!P.mask_in || P.fixed == nullptr || k < 0 || k >= G.pz) return;
-    double* dst = Up + ((k + 3) % 3) * (3 * PN);
-    const int rowlen = 3 * PW;
-    for (int idx = t; idx < 3 * PN; idx += NT) {
-      const int jy = idx / rowlen, r = idx - jy * rowlen;
-      const int gx = x0 - 1 + r / 3, gy = y0 - 1 + jy;
-      if (gx >= 0 && gx < G.px && gy >= 0 && gy < G.py) {
-        if ((P.fixed[G.node(gx, gy, k)] >> (r % 3)) & 1) dst[idx] = 0.0;
-      }
-    }
-  };
-
-  double carry[12];
-#pragma unroll
-  for (int i = 0; i < 12; ++i) carry[i] = 0.0;
   double dot = 0.0;
 
-  load_plane(kz0 - 1);
-  load_plane(kz0);
-  double occ_next = 0.0;
-  if (col_in && kz0 - 1 >= 0 && kz0 - 1 < G.nz) occ_next = P.occ[G.elem(ex, ey, kz0 - 1)];
+  // Balanced persistent split: the work is tiles x pz node planes, flattened
+  // tile-major; CTA b takes the contiguous range [w0, w1) and walks it as
+  // (tile, plane range) pieces.
+  const long long W = (long long)P.ntiles * G.pz;
+  const long long w0 = W * blockIdx.x / gridDim.x, w1 = W * (blockIdx.x + 1) / gridDim.x;
+  for (long long w = w0; w < w1;) {
+    const int tile = (int)(w / G.pz);
+    const int kz0 = (int)(w % G.pz);
+    const int kz1 = (int)min((long long)G.pz, kz0 + (w1 - w));  // owned node planes [kz0, kz1)
+    w += kz1 - kz0;
+    const int x0 = (tile % P.ntx) * (wx - 1);
+    const int y0 = (tile / P.ntx) * (wy - 1);
+    const bool owner = active && tx < wx - 1 && ty < wy - 1 && (x0 + tx) < G.px && (y0 + ty) < G.py;
+    __syncthreads();  // previous piece fully consumed the rings
+    // parts of a staged row inside the grid: node doubles [r_lo, r_hi), element columns [e_lo, e_hi)
+    const int r_lo = 3 * max(0, 1 - x0);
+    const int r_hi = 3 * min(PW, G.px - x0 + 1);
+    const int e_lo = max(0, 1 - x0), e_hi = min(wx, G.nx - x0 + 1);
+    // zero the staged halo outside the grid once (those slots are never written again)
+    for (int jy = warp; jy < PH; jy += NT / 32) {
+      const int gy = y0 - 1 + jy;
+      const bool yin = gy >= 0 && gy < G.py;
+      for (int r = lane; r < 3 * PW; r += 32)
+        if (!yin || r < r_lo || r >= r_hi)
+          for (int b = 0; b < kRing; ++b) Up[b * PS + jy * S + r] = 0.0;
+    }
+    for (int jy = warp; jy < wy; jy += NT / 32) {
+      const int ey = y0 - 1 + jy;
+      const bool yin = ey >= 0 && ey < G.ny;
+      for (int j = lane; j < wx; j += 32)
+        if (!yin || j < e_lo || j >= e_hi)
+          for (int b = 0; b < kRing; ++b) Oc[b * OS + jy * wx + j] = 0.0;
+    }
 
-  for (int k = kz0 - 1; k < kz1; ++k) {
-    cp_async_wait_all();
-    if (k == kz0 - 1) mask_plane(k);
-    mask_plane(k + 1);
-    __syncthreads();
-    if (k + 2 <= kz1) load_plane(k + 2);
-
-    const double occ_e = occ_next;
-    if (col_in && k + 1 >= 0 && k + 1 < G.nz) occ_next = P.occ[G.elem(ex, ey, k + 1)];
-    else occ_next = 0.0;
-
-    // gather the 8 nodes (binary local index b = ox + 2 oy + 4 oz) -> c[3b + a]
-    double c[24];
-    {
-      const double* lo = Up + ((k + 3) % 3) * (3 * PN);
-      const double* hi = Up + ((k + 4) % 3) * (3 * PN);
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int j = 3 * ((ty + (b >> 1)) * PW + tx + (b & 1));
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          c[3 * b + a] = lo[j + a];
-          c[3 * (b + 4) + a] = hi[j + a];
+    // stage node plane k and occupancy layer k (zero-filled outside the grid)
+    auto load_layer = [&](int k) {
+      double* dst = Up + ((k + kRing) % kRing) * PS;
+      const bool kin = k >= 0 && k < G.pz;
+      const double* src = P.u + plane_stride * (kin ? k : 0) + 3LL * (x0 - 1);
+      for (int jy = warp; jy < PH; jy += NT / 32) {
+        const int gy = y0 - 1 + jy;
+        if (gy < 0 || gy >= G.py) continue;
+        const double* srow = src + 3LL * G.px * gy;
+        double* drow = dst + jy * S;
+        for (int r = r_lo + lane; r < r_hi; r += 32) {
+          if (kin) cp_async8(drow + r, srow + r);
+          else drow[r] = 0.0;
         }
       }
-    }
-    // forward Walsh-Hadamard (H^T): butterflies over the x, y, z bits
-#pragma unroll
-    for (int bit = 1; bit < 8; bit <<= 1) {
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        if (b & bit) continue;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          const double v0 = c[3 * b + a], v1 = c[3 * (b | bit) + a];
-          c[3 * b + a] = v0 + v1;
-          c[3 * (b | bit) + a] = v1 - v0;
+      double* odst = Oc + ((k + kRing) % kRing) * OS;
+      const bool lin = k >= 0 && k < G.nz;
+      const double* osrc = P.occ + layer_stride * (lin ? k : 0) + (x0 - 1);
+      for (int jy = warp; jy < wy; jy += NT / 32) {
+        const int ey = y0 - 1 + jy;
+        if (ey < 0 || ey >= G.ny) continue;
+        for (int j = e_lo + lane; j < e_hi; j += 32) {
+          if (lin) cp_async8(odst + jy * wx + j, osrc + (long long)G.nx * ey + j);
+          else odst[jy * wx + j] = 0.0;
         }
       }
-    }
-    double gm[24];
-    modal_apply(M.mh, c, gm);
-    // z-stage of the inverse transform, faces in xy-mode space
-    double face[12];
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const double g0 = occ_e * gm[3 * m + a], g1 = occ_e * gm[3 * (m + 4) + a];
-        face[3 * m + a] = (g0 - g1) + carry[3 * m + a];
-        carry[3 * m + a] = g0 + g1;
+      cp_async_commit();
+    };
+
+    const int j00 = ty * S + 3 * tx;
+    auto gather_face = [&](int k, double (&f)[12]) {
+      const double* pl = Up + ((k + kRing) % kRing) * PS + j00;
+  #pragma unroll
+      for (int b = 0; b < 4; ++b)
+  #pragma unroll
+        for (int a = 0; a < 3; ++a) f[3 * b + a] = pl[(b >> 1) * S + 3 * (b & 1) + a];
+    };
+
+    double carry[12];
+  #pragma unroll
+    for (int i = 0; i < 12; ++i) carry[i] = 0.0;
+    double own[3] = {0.0, 0.0, 0.0};  // u at the owned node of the current plane (dot epilogue)
+    const long long own_node = G.node(min(x0 + tx, G.px - 1), min(y0 + ty, G.py - 1), kz0);
+    double* yrow = P.y + 3 * own_node;
+    const uint8_t* frow = MASKOUT ? P.fixed + own_node : nullptr;
+
+    auto step = [&](int k, const double (&bot)[12], double (&top)[12]) {
+      if (k + kAhead <= kz1 && !(P.debug & 2)) load_layer(k + kAhead);
+      else cp_async_commit();  // keep one group per step
+      gather_face(k + 1, top);
+      double own_next[3];
+      if (DOT) {
+        own_next[0] = top[9];
+        own_next[1] = top[10];
+        own_next[2] = top[11];
       }
-    }
-    if (k >= kz0) {
-      // xy inverse transform: mode (mx,my) -> node (ox,oy)
-#pragma unroll
-      for (int bit = 1; bit < 4; bit <<= 1) {
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          if (b & bit) continue;
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            const double g0 = face[3 * b + a], g1 = face[3 * (b | bit) + a];
-            face[3 * b + a] = g0 - g1;
-            face[3 * (b | bit) + a] = g0 + g1;
-          }
-        }
+      xy_forward(top);
+      const double occ_e = Oc[((k + kRing) % kRing) * OS + (active ? t : 0)];
+      double c[24];
+  #pragma unroll
+      for (int i = 0; i < 12; ++i) {
+        c[i] = bot[i] + top[i];
+        c[12 + i] = top[i] - bot[i];
       }
-      double* xs = Xc + 9 * t;
-#pragma unroll
-      for (int i = 0; i < 9; ++i) xs[i] = face[i];  // nodes (0,0), (1,0), (0,1)
-      __syncthreads();
-      if (owner) {
+      double sc[8];
+  #pragma unroll
+      for (int i = 0; i < 8; ++i) sc[i] = occ_e * M.k[i];
+      double gm[24];
+      modal_apply8(sc, c, gm);
+      double face[12];
+  #pragma unroll
+      for (int i = 0; i < 12; ++i) {
+        face[i] = (gm[i] - gm[12 + i]) + carry[i];
+        carry[i] = gm[i] + gm[12 + i];
+      }
+      const bool out = k >= kz0;
+      double* xs = Xc + (k & 1) * XS;
+      if (out) {
+        xy_inverse(face);
+  #pragma unroll
+        for (int i = 0; i < 9; ++i) xs[9 * t + i] = face[i];  // nodes (0,0), (1,0), (0,1)
+      }
+      cp_async_wait_group<kAhead - 2>();  // plane k+2 (and occupancy k+2) landed
+      if (!(P.debug & 1)) __syncthreads();
+      if (out) {
         // node (x0+tx, y0+ty) = local (1,1) of this column, (0,1) of column
         // tx+1, (1,0) of column ty+1 and (0,0) of column (tx+1, ty+1).
-        const double* e10 = Xc + 9 * (t + 1);
-        const double* e01 = Xc + 9 * (t + wx);
-        const double* e11 = Xc + 9 * (t + wx + 1);
-        const long long n = G.node(x0 + tx, y0 + ty, k);
-        const uint8_t fx = (P.fixed != nullptr) ? P.fixed[n] : 0;
-        const double* us = Up + ((k + 3) % 3) * (3 * PN) + 3 * ((ty + 1) * PW + tx + 1);
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          double v = face[9 + a] + e10[6 + a];
-          v += e01[3 + a];
-          v += e11[a];
-          if (P.mask_out && ((fx >> a) & 1)) v = 0.0;
-          if (P.accumulate) v += P.y[3 * n + a];
-          P.y[3 * n + a] = v;
-          dot = fma(us[a], v, dot);
+        const double* e10 = xs + 9 * (t + 1);
+        const double* e01 = xs + 9 * (t + wx);
+        const double* e11 = xs + 9 * (t + wx + 1);
+        double v[3];
+  #pragma unroll
+        for (int a = 0; a < 3; ++a) v[a] = ((face[9 + a] + e10[6 + a]) + e01[3 + a]) + e11[a];
+        if (owner) {
+          const uint8_t fx = MASKOUT ? *frow : 0;
+  #pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            double w = ((fx >> a) & 1) ? 0.0 : v[a];
+            if (P.accumulate) w += yrow[a];
+            if (!(P.debug & 4)) yrow[a] = w;
+            if (DOT) dot = fma(own[a], w, dot);
+          }
         }
+        yrow += plane_stride;
+        if (MASKOUT) frow += (long long)G.px * G.py;
       }
+      if (DOT) {
+        own[0] = own_next[0];
+        own[1] = own_next[1];
+        own[2] = own_next[2];
+      }
+    };
+
+    for (int j = 0; j < kAhead; ++j) {
+      if (kz0 - 1 + j <= kz1) load_layer(kz0 - 1 + j);
+      else cp_async_commit();
+    }
+    cp_async_wait_group<kAhead - 2>();
+    __syncthreads();
+    double fa[12], fb[12];
+    gather_face(kz0 - 1, fa);
+    if (DOT) {
+      own[0] = fa[9];
+      own[1] = fa[10];
+      own[2] = fa[11];
+    }
+    xy_forward(fa);
+    for (int k = kz0 - 1; k < kz1; k += 2) {
+      step(k, fa, fb);
+      if (k + 1 < kz1) step(k + 1, fb, fa);
     }
   }
-  if (P.dot_partial != nullptr) {
-    const double s = block_sum(dot, red);
-    if (t == 0) P.dot_partial[blockIdx.x + gridDim.x * blockIdx.y] = s;
+  if (DOT) {
+    const double sum = block_sum(dot, red);
+    if (t == 0) P.dot_partial[blockIdx.x] = sum;
   }
 }
 
 // Host-side launch planning -------------------------------------------------
 
 static size_t matvec_smem(int nt, int wx, int wy) {
-  const int PN = (wx + 1) * (wy + 1);
-  return sizeof(double) * (9 * (size_t)PN + 9 * (size_t)nt + nt / 32 + 1);
+  const int PS = (wy + 1) * plane_row_stride(wx);
+  return sizeof(double) * (kRing * (size_t)PS + kRing * (size_t)wx * wy + 2 * 9 * (size_t)(nt + kXcPad) + nt / 32 + 1);
 }
 
-// Pick the tile that minimises (waves x per-CTA work); a CTA's work is
-// (zc + 1) layers of wx*wy element columns.
+static int ctas_per_sm(int nt) { return nt == 256 ? 2 : 1; }
+
+// Tile choice for the persistent balanced split: per-SM time ~ (tile work of
+// all pz planes + one halo layer per piece) x warps / resident CTAs. Redundant
+// halo columns and empty tile parts count as work.
+// TVB_MV_PLAN="nt,wx,wy[,ctas]" overrides (tuning sweeps).
 MatvecPlan plan_matvec(const Grid& g, int num_sms) {
+  if (const char* e = getenv("TVB_MV_PLAN")) {
+    int nt = 0, wx = 0, wy = 0, nc = 0;
+    const int got = sscanf(e, "%d,%d,%d,%d", &nt, &wx, &wy, &nc);
+    if (got >= 3 && (nt == 256 || nt == 384 || nt == 512) && wx * wy <= nt && wx >= 2 && wy >= 2) {
+      const int ntx = (g.px + wx - 2) / (wx - 1), nty = (g.py + wy - 2) / (wy - 1);
+      if (got < 4 || nc < 1) nc = num_sms * ctas_per_sm(nt);
+      return MatvecPlan{nt, wx, wy, ntx, nty, nc, matvec_smem(nt, wx, wy)};
+    }
+  }
   MatvecPlan best{};
   double best_cost = 1e300;
-  const int nt = 256;
-  const int ctas_per_sm = 2;
-  for (int wx = 12; wx <= 64; ++wx) {
-    for (int wy = 3; wx * wy <= nt; ++wy) {
-      if (wx * wy < nt - 32) continue;  // keep warps full
-      const int ntx = (g.px + wx - 2) / (wx - 1);
-      const int nty = (g.py + wy - 2) / (wy - 1);
-      const long long tiles = (long long)ntx * nty;
-      for (int nzc = 1; nzc <= g.pz; ++nzc) {
-        const int zc = (g.pz + nzc - 1) / nzc;
-        const int nzc_eff = (g.pz + zc - 1) / zc;
-        const long long ctas = tiles * nzc_eff;
-        const long long slots = (long long)num_sms * ctas_per_sm;
-        const long long waves = (ctas + slots - 1) / slots;
-        // fill fraction of the last wave still costs a full wave per SM
-        const double cost = (double)waves * (zc + 1) * 1.0 + 0.02 * (double)ctas / slots;
-        if (cost < best_cost) {
+  // wx < 20 loses to short staged rows and frequent warp row-wraps (measured
+  // sweeps, profiles/README.md); nt = 512 never won.
+  for (int nt : {256, 384}) {
+    const int nc = num_sms * ctas_per_sm(nt);
+    for (int wx = 20; wx <= 48; ++wx) {
+      for (int wy = 3; wx * wy <= nt; ++wy) {
+        if (wx * wy < nt - 48) continue;
+        const int ntx = (g.px + wx - 2) / (wx - 1);
+        const int nty = (g.py + wy - 2) / (wy - 1);
+        const double tiles = (double)ntx * nty;
+        const int warps = (wx * wy + 31) / 32;
+        const double pieces = std::max(tiles, (double)nc) + nc;  // upper bound of pieces
+        const double cost = (tiles * g.pz + 1.5 * pieces) * warps / nc / ctas_per_sm(nt);
+        if (cost < best_cost - 1e-9) {
           best_cost = cost;
-          best = MatvecPlan{nt, wx, wy, ntx, nty, nzc_eff, zc, matvec_smem(nt, wx, wy)};
+          best = MatvecPlan{nt, wx, wy, ntx, nty, nc, matvec_smem(nt, wx, wy)};
         }
-        if (ctas > 8 * slots) break;
       }
     }
   }
   return best;
 }
 
+template <int NT, int MINB>
+static void set_smem_attr(size_t bytes) {
+  cudaFuncSetAttribute(k_matvec<NT, MINB, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  cudaFuncSetAttribute(k_matvec<NT, MINB, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  cudaFuncSetAttribute(k_matvec<NT, MINB, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  cudaFuncSetAttribute(k_matvec<NT, MINB, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+template <int NT, int MINB>
+static void launch_nt(dim3 grid, size_t smem, cudaStream_t s, const MatvecParams& P, const Modal& M) {
+  const bool dot = P.dot_partial != nullptr, mo = P.mask_out && P.fixed != nullptr;
+  if (dot && mo) k_matvec<NT, MINB, true, true><<<grid, NT, smem, s>>>(P, M);
+  else if (dot) k_matvec<NT, MINB, true, false><<<grid, NT, smem, s>>>(P, M);
+  else if (mo) k_matvec<NT, MINB, false, true><<<grid, NT, smem, s>>>(P, M);
+  else k_matvec<NT, MINB, false, false><<<grid, NT, smem, s>>>(P, M);
+}
+
 cudaError_t launch_matvec(const MatvecPlan& pl, MatvecParams P, const Modal& M, cudaStream_t s) {
   P.wx = pl.wx;
   P.wy = pl.wy;
   P.ntx = pl.ntx;
-  P.zc = pl.zc;
+  P.ntiles = pl.ntx * pl.nty;
+  if (const char* d = getenv("TVB_MV_DEBUG")) P.debug = atoi(d);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_matvec<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    set_smem_attr<256, 2>(110 * 1024);
+    set_smem_attr<384, 1>(220 * 1024);
+    set_smem_attr<512, 1>(220 * 1024);
     attr_set = true;
   }
-  dim3 grid(pl.ntx * pl.nty, pl.nzc);
-  k_matvec<256><<<grid, 256, pl.smem, s>>>(P, M);
+  dim3 grid(pl.nctas);
+  if (pl.nt == 256) launch_nt<256, 2>(grid, pl.smem, s, P, M);
+  else if (pl.nt == 384) launch_nt<384, 1>(grid, pl.smem, s, P, M);
+  else launch_nt<512, 1>(grid, pl.smem, s, P, M);
   return cudaGetLastError();
 }
 

@@ -14,15 +14,18 @@ struct MatvecParams {
   int accumulate;         // y += A u instead of y = A u
   int wx, wy;             // element columns per tile (incl. 1 halo column/row)
   int ntx;                // tiles along x
-  int zc;                 // owned node planes per CTA
+  int ntiles;             // ntx * nty
+  int debug;              // tuning experiments only (TVB_MV_DEBUG)
   double* dot_partial;    // per-CTA partial of sum(u_owned * y_owned), or nullptr
   const int* stop;        // if non-null and *stop != 0 the launch is a no-op (solver done)
 };
 
+// nt threads per CTA, wx x wy element-column tiles (ntx x nty of them),
+// nctas persistent CTAs each taking an equal share of the tile x plane work.
 struct MatvecPlan {
-  int nt, wx, wy, ntx, nty, nzc, zc;
+  int nt, wx, wy, ntx, nty, nctas;
   size_t smem;
-  int nblocks() const { return ntx * nty * nzc; }
+  int nblocks() const { return nctas; }
 };
 
 MatvecPlan plan_matvec(const Grid& g, int num_sms);
