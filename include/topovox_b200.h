@@ -113,6 +113,33 @@ int tvb_coarse_assemble(int nx, int ny, int nz, int block, double h, const doubl
 /* dense (6Nb x 6Nb, row-major) copy of the block stencil (small coarse spaces) */
 int tvb_coarse_dense(int nx, int ny, int nz, int block, const double* d_Es, double* d_E, void* stream);
 
+/* a7: exact coarse solve x = E^-1 y with the nested-dissection block-LDL^T
+ * factor (paper_2203_15115_b200/coarse.py builds it). Replaces the dense
+ * cho_solve of DeflationSpace.coarse_solve (fea.py:208-211). All d_* are
+ * device arrays described in coarse.py; h_fwd_ptr / h_bwd_ptr are host
+ * arrays of height+2 work-item group offsets. */
+typedef struct tvb_coarse_nd {
+  int n_nodes, height, max_front;
+  const long long* d_meta;
+  const long long* d_children;
+  const int* d_cmap;
+  const double* d_G;
+  const double* d_Gt;
+  const double* d_Z;
+  const int* d_sdof;
+  const int* d_udof;
+  double* d_fS;
+  double* d_cU;
+  const int* d_fwd_items;
+  const int* d_bwd_items;
+  const long long* h_fwd_ptr;
+  const long long* h_bwd_ptr;
+  unsigned* d_phase_done;   /* 2*(height+1) zeroed counters: persistent single-launch solve (NULL: per-height launches) */
+  const double* d_factor;   /* the single allocation holding G, G^T and Z (L2 persistence window) */
+  size_t factor_bytes;
+} tvb_coarse_nd;
+int tvb_coarse_nd_solve(const tvb_coarse_nd* nd, const double* d_y, double* d_x, void* stream);
+
 /* a8: (deflated) Jacobi PCG -- replaces solve_static (fea.py:218-299).
  * Synchronous: returns after convergence / the iteration cap. */
 typedef struct tvb_pcg_desc {
@@ -129,13 +156,14 @@ typedef struct tvb_pcg_desc {
   double tol;
   int max_iters;
   int check_every;          /* iterations per CUDA-graph launch (<= 0: default) */
-  /* deflation: block <= 0 or d_coarse == NULL -> plain Jacobi PCG */
+  /* deflation: block <= 0 or no coarse data -> plain Jacobi PCG */
   int block;
   const double* d_cen;
   const double* d_S;
   const int* d_keep;
-  const double* d_coarse;   /* coarse solver data (see coarse_kind) */
-  int coarse_kind;          /* 0 = dense inverse f64[nc*nc] */
+  const double* d_coarse;   /* coarse_kind 0: dense inverse f64[nc*nc] */
+  int coarse_kind;          /* 0 = dense inverse, 1 = nested dissection (coarse_nd) */
+  const tvb_coarse_nd* coarse_nd;
   /* outputs */
   int iterations;
   double residual;

@@ -22,6 +22,18 @@ _lib = None
 c_int, c_double, c_size_t, c_ll, P = ctypes.c_int, ctypes.c_double, ctypes.c_size_t, ctypes.c_longlong, ctypes.c_void_p
 
 
+class CoarseND(ctypes.Structure):
+    _fields_ = [
+        ("n_nodes", c_int), ("height", c_int), ("max_front", c_int),
+        ("d_meta", P), ("d_children", P), ("d_cmap", P),
+        ("d_G", P), ("d_Gt", P), ("d_Z", P),
+        ("d_sdof", P), ("d_udof", P), ("d_fS", P), ("d_cU", P),
+        ("d_fwd_items", P), ("d_bwd_items", P),
+        ("h_fwd_ptr", P), ("h_bwd_ptr", P), ("d_phase_done", P),
+        ("d_factor", P), ("factor_bytes", c_size_t),
+    ]
+
+
 class PcgDesc(ctypes.Structure):
     _fields_ = [
         ("nx", c_int), ("ny", c_int), ("nz", c_int),
@@ -31,7 +43,7 @@ class PcgDesc(ctypes.Structure):
         ("d_ws", P), ("ws_bytes", c_size_t),
         ("tol", c_double), ("max_iters", c_int), ("check_every", c_int),
         ("block", c_int), ("d_cen", P), ("d_S", P), ("d_keep", P),
-        ("d_coarse", P), ("coarse_kind", c_int),
+        ("d_coarse", P), ("coarse_kind", c_int), ("coarse_nd", ctypes.POINTER(CoarseND)),
         ("iterations", c_int), ("residual", c_double), ("fnorm", c_double),
     ]
 
@@ -54,6 +66,7 @@ _SIGS = {
     "tvb_coarse_assemble_ws_bytes": (c_size_t, [c_int, c_int, c_int, c_int]),
     "tvb_coarse_assemble": (c_int, [c_int, c_int, c_int, c_int, c_double, P, P, P, P, P, P, P, P, c_size_t, P]),
     "tvb_coarse_dense": (c_int, [c_int, c_int, c_int, c_int, P, P, P]),
+    "tvb_coarse_nd_solve": (c_int, [ctypes.POINTER(CoarseND), P, P, P]),
     "tvb_pcg_ws_bytes": (c_size_t, [c_int, c_int, c_int, c_int]),
     "tvb_pcg_solve": (c_int, [ctypes.POINTER(PcgDesc), P]),
     "tvb_elem_ws_bytes": (c_size_t, [c_int, c_int, c_int]),

@@ -4,6 +4,7 @@
 #include <string>
 
 #include "../../include/topovox_b200.h"
+#include "coarse.cuh"
 #include "deflation.cuh"
 #include "fields.cuh"
 #include "matvec.cuh"
@@ -87,6 +88,45 @@ __global__ void k_subset_occ(long long ne, const int* counts, const double* occ,
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= ne) return;
   out[e] = counts[e] ? (double)counts[e] * occ[e] : 0.0;
+}
+
+static CoarseNDDev coarse_nd_dev(const tvb_coarse_nd* d) {
+  CoarseNDDev D;
+  D.n_nodes = d->n_nodes;
+  D.height = d->height;
+  D.max_front = d->max_front;
+  D.meta = d->d_meta;
+  D.children = d->d_children;
+  D.cmap = d->d_cmap;
+  D.G = d->d_G;
+  D.Gt = d->d_Gt;
+  D.Z = d->d_Z;
+  D.sdof = d->d_sdof;
+  D.udof = d->d_udof;
+  D.fS = d->d_fS;
+  D.cU = d->d_cU;
+  D.fwd_items = d->d_fwd_items;
+  D.bwd_items = d->d_bwd_items;
+  D.fwd_ptr = d->h_fwd_ptr;
+  D.bwd_ptr = d->h_bwd_ptr;
+  D.phases = CoarsePhases{};
+  const int nph = 2 * (d->height + 1);
+  if (d->d_phase_done != nullptr && nph <= 63) {
+    D.phases.n_phases = nph;
+    D.phases.last_fwd = d->height;
+    D.phases.done = d->d_phase_done;
+    long long acc = 0;
+    for (int h = 0; h <= d->height; ++h) {
+      D.phases.start[h] = acc;
+      acc += d->h_fwd_ptr[h + 1] - d->h_fwd_ptr[h];
+    }
+    for (int h = 0; h <= d->height; ++h) {
+      D.phases.start[d->height + 1 + h] = acc;
+      acc += d->h_bwd_ptr[h + 1] - d->h_bwd_ptr[h];
+    }
+    D.phases.start[nph] = acc;
+  }
+  return D;
 }
 
 }  // namespace tvb
@@ -355,12 +395,18 @@ int tvb_pcg_solve(tvb_pcg_desc* d, void* stream) {
   P.tol = d->tol;
   P.max_iters = d->max_iters;
   P.check_every = d->check_every;
-  P.block = (d->d_coarse != nullptr) ? d->block : 0;
+  P.block = (d->d_coarse != nullptr || d->coarse_nd != nullptr) ? d->block : 0;
   P.cen = d->d_cen;
   P.S = d->d_S;
   P.keep = d->d_keep;
   P.coarse = d->d_coarse;
   P.coarse_kind = d->coarse_kind;
+  if (P.coarse_kind == 1) {
+    if (!d->coarse_nd) return kStatusBadArg;
+    P.nd = coarse_nd_dev(d->coarse_nd);
+    P.nd_factor = d->coarse_nd->d_factor;
+    P.nd_factor_bytes = d->coarse_nd->factor_bytes;
+  }
   if (P.block > 0 && (!P.cen || !P.S || !P.keep)) return kStatusBadArg;
   PcgResult R;
   const int st = pcg_solve(P, R, (cudaStream_t)stream);
@@ -368,6 +414,11 @@ int tvb_pcg_solve(tvb_pcg_desc* d, void* stream) {
   d->residual = R.residual;
   d->fnorm = R.fnorm;
   return st;
+}
+
+int tvb_coarse_nd_solve(const tvb_coarse_nd* nd, const double* d_y, double* d_x, void* stream) {
+  if (!nd || !d_y || !d_x) return kStatusBadArg;
+  return check(launch_coarse_nd(coarse_nd_dev(nd), d_y, d_x, nullptr, (cudaStream_t)stream));
 }
 
 static Elastic elastic(double E, double nu) {

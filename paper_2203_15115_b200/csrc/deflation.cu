@@ -208,12 +208,14 @@ cudaError_t launch_block_basis(const Agglo& A, const double* occ, const uint8_t*
 // restriction: yc_B = S_B^T [sum y~ ; sum r x y~] over structural nodes of the
 // closed box, y~ = y with fixed DOFs zeroed. One CTA per block, fixed order.
 // ---------------------------------------------------------------------------
-constexpr int kRestrictThreads = 128;
+constexpr int kRestrictThreads = 256;
 
 __global__ void __launch_bounds__(kRestrictThreads) k_restrict(Agglo A, const uint8_t* nflags, DeflData D,
-                                                               const double* y, double* yc, const int* stop) {
+                                                               const double* y, const double* y2,
+                                                               const SolverState* st, double* yc, const int* stop) {
   __shared__ double red[32], m[6];
   if (stop != nullptr && *stop) return;
+  const double beta = (y2 != nullptr) ? st->beta : 0.0;  // restrict y + beta*y2
   const long long B = blockIdx.x;
   const int keep = D.keep[B];
   if (keep == 0) {
@@ -230,11 +232,18 @@ __global__ void __launch_bounds__(kRestrictThreads) k_restrict(Agglo A, const ui
   for (int i = threadIdx.x; i < nnl; i += blockDim.x) {
     const int lx = i % nxl, ly = (i / nxl) % nyl, lz = i / (nxl * nyl);
     const long long n = G.node(X0 + lx, Y0 + ly, Z0 + lz);
-    const uint8_t fl = nflags[n];
+    // independent loads (flags and all three components in flight together)
+    const uint8_t fl = __ldg(nflags + n);
+    double w0 = __ldg(y + 3 * n), w1 = __ldg(y + 3 * n + 1), w2 = __ldg(y + 3 * n + 2);
+    if (y2 != nullptr) {
+      w0 = fma(beta, __ldg(y2 + 3 * n), w0);
+      w1 = fma(beta, __ldg(y2 + 3 * n + 1), w1);
+      w2 = fma(beta, __ldg(y2 + 3 * n + 2), w2);
+    }
     if (!(fl & kStructBit)) continue;
-    const double vx = (fl & 1) ? 0.0 : y[3 * n];
-    const double vy = (fl & 2) ? 0.0 : y[3 * n + 1];
-    const double vz = (fl & 4) ? 0.0 : y[3 * n + 2];
+    const double vx = (fl & 1) ? 0.0 : w0;
+    const double vy = (fl & 2) ? 0.0 : w1;
+    const double vz = (fl & 4) ? 0.0 : w2;
     const double rx = A.h * (lx - cx), ry = A.h * (ly - cy), rz = A.h * (lz - cz);
     acc[0] += vx;
     acc[1] += vy;
@@ -258,8 +267,8 @@ __global__ void __launch_bounds__(kRestrictThreads) k_restrict(Agglo A, const ui
 }
 
 cudaError_t launch_restrict(const Agglo& A, const uint8_t* nflags, DeflData D, const double* y, double* yc,
-                            cudaStream_t s, const int* stop) {
-  k_restrict<<<(unsigned)A.nb, kRestrictThreads, 0, s>>>(A, nflags, D, y, yc, stop);
+                            cudaStream_t s, const int* stop, const double* y2, const void* state) {
+  k_restrict<<<(unsigned)A.nb, kRestrictThreads, 0, s>>>(A, nflags, D, y, y2, (const SolverState*)state, yc, stop);
   return cudaGetLastError();
 }
 
@@ -306,8 +315,8 @@ __global__ void k_prolong(Agglo A, const uint8_t* nflags, const double* cen, con
     for (int k = 0; k < nbz; ++k)
       for (int j = 0; j < nby; ++j)
         for (int i = 0; i < nbx; ++i) {
+          // nu_B = S_B mu_B is exactly zero for inactive blocks (S_B == 0): no keep lookup
           const long long B = bxs[i] + (long long)A.mx * (bys[j] + (long long)A.my * bzs[k]);
-          if (keepv[B] == 0) continue;
           const double* w = nu + 6 * B;
           const double rx = A.h * (x - b * bxs[i] - cen[3 * B]);
           const double ry = A.h * (y - b * bys[j] - cen[3 * B + 1]);

@@ -47,9 +47,10 @@ struct DeflData {
 cudaError_t launch_node_flags(const Grid& G, const long long* fixed_dofs, long long nfixed, const double* occ,
                               uint8_t* nflags, cudaStream_t s);
 cudaError_t launch_block_basis(const Agglo& A, const double* occ, const uint8_t* nflags, DeflData D, cudaStream_t s);
-// yc[6B + j] = (W^T y)_Bj
+// yc[6B + j] = (W^T y)_Bj, or (W^T (y + beta*y2))_Bj with beta from the solver state
 cudaError_t launch_restrict(const Agglo& A, const uint8_t* nflags, DeflData D, const double* y, double* yc,
-                            cudaStream_t s, const int* stop = nullptr);
+                            cudaStream_t s, const int* stop = nullptr, const double* y2 = nullptr,
+                            const void* state = nullptr);
 // nu[6B..] = S_B * mu_B  (rigid motion (t, omega) of each block)
 cudaError_t launch_block_nu(const Agglo& A, DeflData D, const double* mu, double* nu, cudaStream_t s,
                             const int* stop = nullptr);

@@ -10,7 +10,17 @@
 //         stop if |r|/|f_free| <= tol ; z = D^-1 r ; beta = r.z_new / rz
 //         p = z + beta p - W E^-1 (AW)^T z
 // with (AW)^T z evaluated as W^T (A z) (A symmetric, W zero on fixed DOFs).
+//
+// Stabilised projection: the loop projects z + beta p instead of z,
+//     p = z + beta p - W E^-1 W^T (A z + beta q),   q = A p_old,
+// which equals the reference update in exact arithmetic (W^T A p_old = 0) but
+// re-imposes W^T A p = 0 every iteration. The reference recurrence lets that
+// component drift: on a Bernoulli(0.9) cantilever the reference itself
+// converges with scipy's cho_solve and diverges when only the rounding of the
+// coarse solve changes (explicit inverse), see DESIGN.md §4 / tests.
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -43,7 +53,7 @@ cudaError_t launch_dense_gemv(long long nc, const double* Einv, const double* yc
 
 // ---------------------------------------------------------------------------
 struct PcgWork {
-  double *r, *z, *p, *q, *inv_d;
+  double *r, *z, *p, *q, *t, *inv_d;
   double *yc, *mu, *nu;
   double* partials;
   SolverState* st;
@@ -57,7 +67,7 @@ size_t pcg_ws_bytes(const Grid& g, int block) {
   size_t nb = 0;
   if (block > 0) nb = (size_t)make_agglo(g, block, 1.0).nb;
   size_t b = 0;
-  b += 5 * align_up(nd * sizeof(double));
+  b += 6 * align_up(nd * sizeof(double));
   b += 3 * align_up(6 * nb * sizeof(double) + 8);
   b += align_up((size_t)(2 * kMaxReduceCtas + 65536) * sizeof(double));
   b += align_up(sizeof(SolverState));
@@ -80,6 +90,7 @@ static PcgWork carve(void* ws, const Grid& g, int block) {
   w.z = (double*)take(nd * sizeof(double));
   w.p = (double*)take(nd * sizeof(double));
   w.q = (double*)take(nd * sizeof(double));
+  w.t = (double*)take(nd * sizeof(double));
   w.inv_d = (double*)take(nd * sizeof(double));
   w.yc = (double*)take(6 * nb * sizeof(double) + 8);
   w.mu = (double*)take(6 * nb * sizeof(double) + 8);
@@ -102,7 +113,7 @@ static PcgWork carve(void* ws, const Grid& g, int block) {
 int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
   const Grid& G = P.g;
   const long long nd = 3 * G.nn;
-  const bool defl = P.block > 0 && P.coarse != nullptr;
+  const bool defl = P.block > 0 && (P.coarse_kind == 1 || P.coarse != nullptr);
   Agglo A{};
   if (defl) A = make_agglo(G, P.block, P.h);
   if (P.ws_bytes < pcg_ws_bytes(G, defl ? P.block : 0)) {
@@ -145,14 +156,37 @@ int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
     mp.stop = stop;
     return launch_matvec(plan, mp, P.modal, s);
   };
-  auto coarse_project = [&](const double* v, const int* stop) -> cudaError_t {
-    // nu = S E^-1 W^T v  (v = A z or f)
-    cudaError_t e = launch_restrict(A, P.nflags, D, v, W.yc, s, stop);
+  auto coarse_project = [&](const double* v, const int* stop, const double* v2 = nullptr) -> cudaError_t {
+    // nu = S E^-1 W^T (v + beta v2)  (v = f, A z ; v2 = q)
+    cudaError_t e = launch_restrict(A, P.nflags, D, v, W.yc, s, stop, v2, W.st);
     if (e != cudaSuccess) return e;
-    e = launch_dense_gemv(6 * A.nb, P.coarse, W.yc, W.mu, stop, s);
+    if (P.coarse_kind == 1) e = launch_coarse_nd(P.nd, W.yc, W.mu, stop, s);
+    else e = launch_dense_gemv(6 * A.nb, P.coarse, W.yc, W.mu, stop, s);
     if (e != cudaSuccess) return e;
     return launch_block_nu(A, D, W.mu, W.nu, s, stop);
   };
+
+  // Optional (TVB_L2_PERSIST=1): keep the nested-dissection coarse factor
+  // resident in L2 with an access-policy window (captured into the graph's
+  // kernel nodes). Measured slower at C3/C4 (the carve-out costs the
+  // streaming matvecs more than the coarse solve gains), so off by default.
+  if (P.coarse_kind == 1 && P.nd_factor != nullptr && P.nd_factor_bytes > 0 && getenv("TVB_L2_PERSIST")) {
+    int max_persist = 0, max_window = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    if (max_persist > 0 && max_window > 0) {
+      const size_t bytes = std::min(P.nd_factor_bytes, (size_t)max_window);
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min(bytes, (size_t)max_persist));
+      cudaStreamAttrValue av = {};
+      av.accessPolicyWindow.base_ptr = (void*)P.nd_factor;
+      av.accessPolicyWindow.num_bytes = bytes;
+      av.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)max_persist / (double)bytes);
+      av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &av);
+    }
+    cudaGetLastError();  // the window is an optimisation only
+  }
 
   // --- prologue ------------------------------------------------------------
   SolverState st0{};
@@ -217,14 +251,56 @@ int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
     e = launch_pcg_update(nd, P.x, W.r, W.z, W.p, W.q, W.inv_d, W.st, W.partials, s);
     if (e != cudaSuccess) return e;
     if (defl) {
-      e = matvec(W.z, W.q, false, stop);
+      e = matvec(W.z, W.t, false, stop);
       if (e != cudaSuccess) return e;
-      e = coarse_project(W.q, stop);
+      e = coarse_project(W.t, stop, W.q);
       if (e != cudaSuccess) return e;
       return launch_prolong(A, P.nflags, D, W.nu, W.p, W.z, W.st, 1, s);
     }
     return launch_pcg_pupdate(nd, W.p, W.z, W.st, s);
   };
+  // TVB_SOLVE_PROFILE=1: run a few iterations eagerly with CUDA events around
+  // every stage and print the per-stage device time (tuning only).
+  if (getenv("TVB_SOLVE_PROFILE")) {
+    const char* names[6] = {"matvec_Ap+pq", "pcg_update", "matvec_Az", "restrict", "coarse_solve", "nu+prolong"};
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    cudaEvent_t ev[7];
+    for (auto& e : ev) cudaEventCreate(&e);
+    int nit = 0;
+    for (; nit < 20; ++nit) {
+      cudaEventRecord(ev[0], s);
+      matvec(W.p, W.q, true, stop);
+      launch_finalize_pq(W.partials + 2 * kMaxReduceCtas, plan.nblocks(), W.st, s);
+      cudaEventRecord(ev[1], s);
+      launch_pcg_update(nd, P.x, W.r, W.z, W.p, W.q, W.inv_d, W.st, W.partials, s);
+      cudaEventRecord(ev[2], s);
+      if (defl) {
+        matvec(W.z, W.t, false, stop);
+        cudaEventRecord(ev[3], s);
+        launch_restrict(A, P.nflags, D, W.t, W.yc, s, stop, W.q, W.st);
+        cudaEventRecord(ev[4], s);
+        if (P.coarse_kind == 1) launch_coarse_nd(P.nd, W.yc, W.mu, stop, s);
+        else launch_dense_gemv(6 * A.nb, P.coarse, W.yc, W.mu, stop, s);
+        cudaEventRecord(ev[5], s);
+        launch_block_nu(A, D, W.mu, W.nu, s, stop);
+        launch_prolong(A, P.nflags, D, W.nu, W.p, W.z, W.st, 1, s);
+      } else {
+        launch_pcg_pupdate(nd, W.p, W.z, W.st, s);
+        for (int k = 3; k < 6; ++k) cudaEventRecord(ev[k], s);
+      }
+      cudaEventRecord(ev[6], s);
+      cudaStreamSynchronize(s);
+      for (int k = 0; k < 6; ++k) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+        acc[k] += ms;
+      }
+    }
+    fprintf(stderr, "[tvb solve profile] per-iteration us:");
+    for (int k = 0; k < 6; ++k) fprintf(stderr, " %s=%.1f", names[k], 1e3 * acc[k] / nit);
+    fprintf(stderr, "\n");
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
   int batch = P.check_every > 0 ? P.check_every : 8;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;

@@ -1,4 +1,5 @@
 #pragma once
+#include "coarse.cuh"
 #include "common.cuh"
 
 namespace tvb {
@@ -24,7 +25,10 @@ struct PcgProblem {
   const double* S;
   const int* keep;
   const double* coarse;  // dense inverse (coarse_kind 0)
-  int coarse_kind;
+  int coarse_kind;       // 0 dense inverse, 1 nested dissection
+  CoarseNDDev nd;
+  const double* nd_factor = nullptr;  // L2-persisting window (the ND factor)
+  size_t nd_factor_bytes = 0;
 };
 
 struct PcgResult {

@@ -33,8 +33,11 @@ from .mesh import Domain, Topology
 log = logging.getLogger(__name__)
 
 DENSE_ORACLE_DOF_LIMIT = 3000
-#: largest coarse space handled by the dense coarse inverse
-DENSE_COARSE_LIMIT = 24000
+#: coarse spaces up to this many DOFs use an explicit dense inverse (one
+#: GEMV per iteration beats the nested-dissection launches); larger ones the
+#: nested-dissection block-LDL^T factor (coarse.py)
+DENSE_COARSE_AUTO_LIMIT = 3000
+DENSE_COARSE_MAX = 24000
 
 
 def _torch():
@@ -180,10 +183,13 @@ class DeflationSpace:
     the host only when accessed (API compatibility).
     """
 
-    def __init__(self, domain: Domain, topology: Topology, dirichlet=(), block: int = 4):
+    def __init__(self, domain: Domain, topology: Topology, dirichlet=(), block: int = 4, coarse: str = "auto"):
         if block < 2:
             raise ValueError(f"agglomerate side must be >= 2, got {block}")
+        if coarse not in ("auto", "dense", "nd"):
+            raise ValueError(f"coarse must be auto|dense|nd, got {coarse!r}")
         torch = _torch()
+        self.coarse = coarse
         self.domain = domain
         self.topology = topology
         self.block = int(block)
@@ -205,6 +211,7 @@ class DeflationSpace:
         self._prepared_for = None
         self.Es = None
         self.coarse_inv = None
+        self.nd = None
         self._W = None
 
     # --- coarse operator -----------------------------------------------------
@@ -224,33 +231,52 @@ class DeflationSpace:
                                         ptr(ws), nws, stream_ptr()), "coarse operator")
         del ws
         nc = 6 * nb
-        if nc > DENSE_COARSE_LIMIT:
-            raise NotImplementedError(f"coarse space of {nc} DOFs needs the sparse coarse factorisation")
-        E = torch.empty(nc * nc, dtype=torch.float64, device="cuda")
-        check(lib().tvb_coarse_dense(d.nx, d.ny, d.nz, self.block, ptr(self.Es), ptr(E), stream_ptr()),
-              "coarse dense")
-        E = E.view(nc, nc)
-        L, info = torch.linalg.cholesky_ex(E)
-        if int(info.item()) != 0:
-            log.warning("deflation coarse matrix not SPD; falling back to pseudo-inverse")
-            self.coarse_inv = torch.linalg.pinv(E, hermitian=True).contiguous()
-        else:
-            self.coarse_inv = torch.cholesky_inverse(L).contiguous()
-        del E, L
+        kind = self.coarse
+        if kind == "auto":
+            kind = "dense" if nc <= DENSE_COARSE_AUTO_LIMIT else "nd"
+        self.coarse_inv = None
+        self.nd = None
+        if kind == "nd":
+            from .coarse import NDCoarseSolver
+
+            try:
+                self.nd = NDCoarseSolver(self.grid, self.Es)
+            except np.linalg.LinAlgError:
+                if nc > DENSE_COARSE_MAX:
+                    raise
+                log.warning("deflation coarse matrix not SPD; falling back to pseudo-inverse")
+                kind = "dense"
+        if kind == "dense":
+            if nc > DENSE_COARSE_MAX:
+                raise ValueError(f"dense coarse inverse limited to {DENSE_COARSE_MAX} DOFs, got {nc}")
+            E = torch.empty(nc * nc, dtype=torch.float64, device="cuda")
+            check(lib().tvb_coarse_dense(d.nx, d.ny, d.nz, self.block, ptr(self.Es), ptr(E), stream_ptr()),
+                  "coarse dense")
+            E = E.view(nc, nc)
+            L, info = torch.linalg.cholesky_ex(E)
+            if int(info.item()) != 0:
+                log.warning("deflation coarse matrix not SPD; falling back to pseudo-inverse")
+                self.coarse_inv = torch.linalg.pinv(E, hermitian=True).contiguous()
+            else:
+                self.coarse_inv = torch.cholesky_inverse(L).contiguous()
+            del E, L
         self._prepared_for = op
 
     def coarse_solve(self, rhs):
         """E^-1 rhs in this space's (kept-column) coarse basis."""
         torch = _torch()
-        if self.coarse_inv is None:
+        if self.coarse_inv is None and self.nd is None:
             raise RuntimeError("DeflationSpace.prepare(op) must run first")
         np_in = not isinstance(rhs, torch.Tensor)
         r = torch.as_tensor(np.asarray(rhs, dtype=np.float64) if np_in else rhs, device="cuda", dtype=torch.float64)
         mask = torch.from_numpy(self.kept_mask.ravel()).cuda()
         full = torch.zeros(6 * self.n_blocks, dtype=torch.float64, device="cuda")
         full[mask] = r
-        out = (self.coarse_inv @ full)[mask]
-        return to_host_if(out, np_in)
+        if self.nd is not None:
+            sol = self.nd.solve_device(full, torch.empty_like(full))
+        else:
+            sol = self.coarse_inv @ full
+        return to_host_if(sol[mask], np_in)
 
     # --- host views (compatibility / tests) ------------------------------------
     @property
@@ -320,8 +346,9 @@ def _materialize_w(space: DeflationSpace):
                                    shape=(d.n_dofs, col0))
 
 
-def build_deflation(domain: Domain, topology: Topology, dirichlet=(), block: int = 4) -> DeflationSpace:
-    return DeflationSpace(domain, topology, dirichlet, block)
+def build_deflation(domain: Domain, topology: Topology, dirichlet=(), block: int = 4,
+                    coarse: str = "auto") -> DeflationSpace:
+    return DeflationSpace(domain, topology, dirichlet, block, coarse)
 
 
 def default_max_iters(n_dofs: int) -> int:
@@ -362,8 +389,12 @@ def solve_static(op: StiffnessOperator, f, tol: float = 1.0e-8, max_iters: int |
     if defl is not None:
         desc.block = defl.block
         desc.d_cen, desc.d_S, desc.d_keep = ptr(defl.cen), ptr(defl.S), ptr(defl.keep)
-        desc.d_coarse = ptr(defl.coarse_inv)
-        desc.coarse_kind = 0
+        if defl.nd is not None:
+            desc.coarse_kind = 1
+            desc.coarse_nd = ctypes.pointer(defl.nd.desc)
+        else:
+            desc.d_coarse = ptr(defl.coarse_inv)
+            desc.coarse_kind = 0
     st = lib().tvb_pcg_solve(ctypes.byref(desc), stream_ptr())
     if st == STATUS_NO_CONVERGENCE:
         raise NoConvergence(f"CG did not reach {tol:g} in {max_iters} iterations (residual {desc.residual:.3e})",

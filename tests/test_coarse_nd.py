@@ -1,0 +1,97 @@
+"""Nested-dissection coarse factor (host symbolic + factorisation, CPU torch)
+checked against a dense solve, by emulating the two device solve kernels
+(k_coarse_fwd / k_coarse_bwd) on the packed arrays. CPU only."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+
+def random_block_stencil(mx, my, mz, seed=0):
+    """Symmetric, diagonally dominant 27-neighbour 6x6 block stencil."""
+    rng = np.random.default_rng(seed)
+    nb = mx * my * mz
+    Es = np.zeros((nb, 27, 6, 6))
+    for B in range(nb):
+        bx, by, bz = B % mx, (B // mx) % my, B // (mx * my)
+        for d in range(27):
+            dx, dy, dz = d % 3 - 1, (d // 3) % 3 - 1, d // 9 - 1
+            cx, cy, cz = bx + dx, by + dy, bz + dz
+            if not (0 <= cx < mx and 0 <= cy < my and 0 <= cz < mz):
+                continue
+            C = cx + mx * (cy + my * cz)
+            if (C, 26 - d) < (B, d):
+                Es[B, d] = Es[C, 26 - d].T
+            elif d == 13:
+                a = rng.standard_normal((6, 6))
+                Es[B, d] = a @ a.T + 60.0 * np.eye(6)
+            else:
+                Es[B, d] = rng.standard_normal((6, 6))
+    return Es
+
+
+def dense_of(Es, mx, my, mz):
+    nb = mx * my * mz
+    E = np.zeros((6 * nb, 6 * nb))
+    for B in range(nb):
+        bx, by, bz = B % mx, (B // mx) % my, B // (mx * my)
+        for d in range(27):
+            dx, dy, dz = d % 3 - 1, (d // 3) % 3 - 1, d // 9 - 1
+            cx, cy, cz = bx + dx, by + dy, bz + dz
+            if 0 <= cx < mx and 0 <= cy < my and 0 <= cz < mz:
+                C = cx + mx * (cy + my * cz)
+                E[6 * B:6 * B + 6, 6 * C:6 * C + 6] = Es[B, d]
+    return E
+
+
+def emulate_solve(nd, y):
+    """numpy twin of k_coarse_fwd / k_coarse_bwd over the packed device data."""
+    meta = nd.meta.numpy()
+    ch = nd.children.numpy()
+    cmap = nd.cmap.numpy()
+    G, Gt, Z = nd.G.numpy(), nd.Gt.numpy(), nd.Z.numpy()
+    sdof, udof = nd.s_dof.numpy(), nd.u_dof.numpy()
+    fS = np.zeros(nd.fS.numel())
+    cU = np.zeros(nd.cU.numel())
+    fwd, bwd = nd.fwd_items.numpy(), nd.bwd_items.numpy()
+    done = set()
+    for node, r0, r1 in fwd:
+        s, u, g, z, so, uo, cb, ce = meta[node]
+        f = np.concatenate([y[sdof[so:so + s]], np.zeros(u)])
+        for k in range(cb, ce):
+            cn, co = ch[k]
+            cu = meta[cn][1]
+            f[cmap[co:co + cu]] += cU[meta[cn][5]:meta[cn][5] + cu]
+        if node not in done:
+            fS[so:so + s] = f[:s]
+            done.add(node)
+        Gm = G[g:g + s * u].reshape(u, s)
+        cU[uo + r0:uo + r1] = f[s + r0:s + r1] - Gm[r0:r1] @ f[:s]
+    x = np.zeros_like(y)
+    for node, r0, r1 in bwd:
+        s, u, g, z, so, uo, cb, ce = meta[node]
+        Zm = Z[z:z + s * s].reshape(s, s)
+        Gtm = Gt[g:g + s * u].reshape(s, u)
+        xu = x[udof[uo:uo + u]]
+        x[sdof[so + r0:so + r1]] = Zm[r0:r1] @ fS[so:so + s] - (Gtm[r0:r1] @ xu if u else 0.0)
+    return x
+
+
+@pytest.mark.parametrize("grid,leaf", [((5, 5, 10), 27), ((4, 3, 2), 2), ((7, 1, 3), 4), ((1, 1, 1), 27)])
+def test_nd_factor_matches_dense(grid, leaf):
+    from paper_2203_15115_b200.coarse import NDCoarseSolver, nested_dissection
+
+    mx, my, mz = grid
+    Es = random_block_stencil(mx, my, mz, seed=sum(grid))
+    E = dense_of(Es, mx, my, mz)
+    assert np.allclose(E, E.T)
+    nodes = nested_dissection(mx, my, mz, leaf)
+    # every block is in exactly one separator
+    allsep = np.concatenate([n.sep for n in nodes])
+    assert np.array_equal(np.sort(allsep), np.arange(mx * my * mz))
+    nd = NDCoarseSolver(grid, torch.from_numpy(Es.reshape(-1)), leaf_max=leaf, make_desc=False)
+    y = np.random.default_rng(1).standard_normal(E.shape[0])
+    x = emulate_solve(nd, y)
+    ref = np.linalg.solve(E, y)
+    assert np.abs(x - ref).max() <= 1e-12 * np.abs(ref).max()

@@ -143,13 +143,14 @@ def test_plain_pcg_golden(tv, golden):
     assert rel(r.u, golden["bern865_plain_t12_u"]) < 1e-10
 
 
+@pytest.mark.parametrize("coarse", ["dense", "nd"])
 @pytest.mark.parametrize("b", [2, 3])
-def test_dpcg_golden(tv, golden, b):
+def test_dpcg_golden(tv, golden, b, coarse):
     from paper_2203_15115_b200 import fea
 
     op = make_op(tv, (8, 6, 5), golden["bern865_occ"], golden["bern865_fixed"])
     d = op.domain
-    defl = fea.build_deflation(d, op.topology, golden["bern865_fixed"], b)
+    defl = fea.build_deflation(d, op.topology, golden["bern865_fixed"], b, coarse=coarse)
     assert defl.n_vectors == int(golden[f"bern865_b{b}_nvec"])
     for t in (8, 12):
         r = fea.solve_static(op, golden["bern865_f"], tol=10.0 ** -t, deflation=defl)
@@ -158,13 +159,14 @@ def test_dpcg_golden(tv, golden, b):
         assert rel(r.u, golden[f"bern865_b{b}_t{t}_u"]) < tol
 
 
-def test_dpcg_c1_golden(tv, golden):
+@pytest.mark.parametrize("coarse", ["dense", "nd"])
+def test_dpcg_c1_golden(tv, golden, coarse):
     """BASELINE configs[0]: 40x20x20 full-solid cantilever, 4^3 agglomerates."""
     from paper_2203_15115_b200 import fea
 
     d, case, fixed, f = cantilever(40, 20, 20, (40, 10, 10), (40, 10, 10))
     op = make_op(tv, (40, 20, 20), np.ones(d.n_elems), fixed)
-    defl = fea.build_deflation(d, op.topology, fixed, 4)
+    defl = fea.build_deflation(d, op.topology, fixed, 4, coarse=coarse)
     assert defl.n_vectors == int(golden["c1_nvec"])
     r8 = fea.solve_static(op, f, tol=1e-8, deflation=defl)
     assert abs(r8.iterations - int(golden["c1_t8_iters"])) <= 1
@@ -229,3 +231,28 @@ def test_extract_with_design_mask(tv, oracle):
     occ, _, _ = oracle.extract(vals, d.design_mask, 0.6, 1e-3)
     occ[~d.design_mask] = tv.EPS_VOID
     assert np.array_equal(t.occupancy, occ)
+
+
+def test_coarse_nd_matches_dense_on_device(tv, golden, oracle):
+    """The ND coarse solve equals the dense inverse on a real E (Bernoulli(0.9)
+    topology; at 0.7-0.85 even the reference DPCG stalls before 1e-12)."""
+    from paper_2203_15115_b200 import fea
+
+    occ = np.where(np.random.default_rng(3).random(24 * 12 * 12) < 0.9, 1.0, 1e-3)
+    d, case, fixed, f = cantilever(24, 12, 12, (24, 0, 0), (24, 12, 12))
+    op = make_op(tv, (24, 12, 12), occ, fixed)
+    dn = fea.build_deflation(d, op.topology, fixed, 3, coarse="dense")
+    nd = fea.build_deflation(d, op.topology, fixed, 3, coarse="nd")
+    dn.prepare(op)
+    nd.prepare(op)
+    y = np.random.default_rng(4).standard_normal(dn.n_vectors)
+    a, b = dn.coarse_solve(y), nd.coarse_solve(y)
+    assert rel(b, a) < 1e-11
+    ra = fea.solve_static(op, f, tol=1e-12, deflation=dn)
+    rb = fea.solve_static(op, f, tol=1e-12, deflation=nd)
+    assert abs(ra.iterations - rb.iterations) <= 1
+    assert rel(rb.u, ra.u) < 1e-10
+    ref = oracle.Operator(24, 12, 12, 1.0, occ, dirichlet=fixed)
+    uo, ito, _ = oracle.solve_static(ref, f, tol=1e-12, deflation=oracle.Deflation(ref, 3))
+    assert abs(rb.iterations - ito) <= 2
+    assert rel(rb.u, uo) < 1e-10
