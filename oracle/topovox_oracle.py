@@ -475,3 +475,93 @@ def update_penalty(gamma, g_prev, g_new, k, varsigma=0.25, eta=10.0):
     if min(g_new, 0.0) <= varsigma * min(g_prev, 0.0):
         return gamma
     return max(eta * gamma, float(k * k))
+
+
+# ---------------------------------------------------------------------------
+# optimizer loop (SPEC.md:146-154 fixed point, SPEC.md:237-246 run), restated
+# independently for whole-run checks on small grids. Constraints: compliance
+# and p-norm stress per load case (the SPEC kinds used by the configs).
+# ---------------------------------------------------------------------------
+def _analyses(nx, ny, nz, occ, cases, specs, E, nu, tol, block, need_fields=True):
+    """cases: list of (fixed_dofs, f); specs: list of dicts(kind, alpha, soft, case, p)."""
+    out = {"q": {}, "fields": {}, "J": 0.0}
+    for ci, (fixed, f) in enumerate(cases):
+        op = Operator(nx, ny, nz, 1.0, occ, E=E, nu=nu, dirichlet=fixed)
+        defl = Deflation(op, block) if block else None
+        u, _, _ = solve_static(op, f, tol=tol, deflation=defl)
+        J = float(f @ u)
+        out["J"] += J
+        strains, stresses, vm = batch_element_state(op, u)
+        for i, s in enumerate(specs):
+            if s["case"] != ci:
+                continue
+            if s["kind"] == "compliance":
+                out["q"][i] = J
+                out["fields"][i] = compliance_sensitivity(strains, stresses, nu)
+            elif s["kind"] == "pnorm_stress":
+                out["q"][i] = pnorm_stress(vm, op.occ, s["p"])
+                if need_fields:
+                    lam, _, _ = solve_static(op, stress_adjoint_rhs(op, u, s["p"]), tol=tol, deflation=defl)
+                    ls, _, _ = batch_element_state(op, lam)
+                    out["fields"][i] = stress_sensitivity(stresses, ls, nu)
+    return out
+
+
+def run_optimizer(nx, ny, nz, cases, specs, E=1.0, nu=0.3, tol=1e-8, block=4, ersatz=1e-6, mu0=100.0, gamma0=10.0,
+                  varsigma=0.25, eta=10.0, dv0=0.025, dv_min=0.005, growth=1.1, growth_after=3, inner_cap=10,
+                  ctol=0.01, ttol=0.001, feas=1e-6, max_outer=400):
+    """Returns (occ, history list of dicts, reason)."""
+    ne = nx * ny * nz
+    design = np.ones(ne, dtype=bool)
+    occ = np.ones(ne)
+    base = _analyses(nx, ny, nz, occ, cases, specs, E, nu, tol, block)
+    q0 = dict(base["q"])
+    gfun = lambda q: {i: constraint_g(q[i], q0[i], s["alpha"], "upper") for i, s in enumerate(specs)}  # noqa: E731
+    g = gfun(base["q"])
+    mu = {i: mu0 for i in range(len(specs))}
+    gam = {i: gamma0 for i in range(len(specs))}
+    acc_occ, acc = occ, base
+    dv, streak, hist, reason = dv0, 0, [], "max_outer"
+    fb = next((i for i, s in enumerate(specs) if s["kind"] == "compliance"), 0)
+    for k in range(1, max_outer + 1):
+        v = float(np.count_nonzero(acc_occ == 1.0)) / ne
+        target = v - dv
+        if target <= 1.0 / ne:
+            reason = "minimum volume reached"
+            break
+        w = {i: max(mu[i] + gam[i] * g[i], 0.0) for i in range(len(specs))}
+        cur, cur_occ = acc, acc_occ
+        conv, inner = False, 0
+        for it in range(1, inner_cap + 1):
+            inner = it
+            ls, _ = combine([cur["fields"][i] for i in range(len(specs))], [w[i] for i in range(len(specs))],
+                            fallback=fb)
+            new_occ, _, _ = extract(ls, design, target, ersatz)
+            if it > 1 and np.count_nonzero((new_occ == 1.0) != (cur_occ == 1.0)) < ttol * ne:
+                conv = True
+                break
+            nxt = _analyses(nx, ny, nz, new_occ, cases, specs, E, nu, tol, block)
+            if it > 1 and abs(nxt["J"] - cur["J"]) < ctol * cur["J"]:
+                cur, cur_occ, conv = nxt, new_occ, True
+                break
+            cur, cur_occ = nxt, new_occ
+        g_new = gfun(cur["q"])
+        hard = any((not s.get("soft", False)) and g_new[i] > feas for i, s in enumerate(specs))
+        hist.append({"k": k, "v": float(np.count_nonzero(cur_occ == 1.0)) / ne, "dv": dv, "accepted": not hard,
+                     "g": dict(g_new), "J": cur["J"], "inner": inner})
+        if hard:
+            dv *= 0.5
+            streak = 0
+            if dv < dv_min:
+                reason = "volume step below dv_min with a hard constraint violated"
+                break
+            continue
+        for i in range(len(specs)):
+            nm = update_multiplier(mu[i], gam[i], g_new[i])
+            gam[i] = update_penalty(gam[i], g[i], g_new[i], k, varsigma, eta)
+            mu[i] = nm
+        g, acc, acc_occ = g_new, cur, cur_occ
+        streak += 1
+        if streak >= growth_after:
+            dv = min(dv * growth, dv0)
+    return acc_occ, hist, reason

@@ -73,8 +73,9 @@ __device__ __forceinline__ void warp_dot4(const double* __restrict__ a0, long lo
 #pragma unroll
     for (int r = 0; r < 4; ++r) s[r] = fma(__ldg(a[r] + i), bk, s[r]);
   }
+  // warp_sum leaves the total in lane 0; broadcast so lane r can store row r
 #pragma unroll
-  for (int r = 0; r < 4; ++r) out[r] = warp_sum(s[r]);
+  for (int r = 0; r < 4; ++r) out[r] = __shfl_sync(0xffffffffu, warp_sum(s[r]), 0);
 }
 
 __device__ __forceinline__ void fwd_item(const CoarseNDDev& D, const int* it, const double* y, double* f) {
