@@ -134,9 +134,12 @@ typedef struct tvb_coarse_nd {
   const int* d_bwd_items;
   const long long* h_fwd_ptr;
   const long long* h_bwd_ptr;
-  unsigned* d_phase_done;   /* 2*(height+1) zeroed counters: persistent single-launch solve (NULL: per-height launches) */
   const double* d_factor;   /* the single allocation holding G, G^T and Z (L2 persistence window) */
   size_t factor_bytes;
+  const int* h_split;       /* per height: 1 = separate front-assembly launch (large fronts) */
+  const int* d_asm_nodes;   /* nodes grouped by height */
+  const long long* h_asm_ptr;
+  int max_sep;
 } tvb_coarse_nd;
 int tvb_coarse_nd_solve(const tvb_coarse_nd* nd, const double* d_y, double* d_x, void* stream);
 

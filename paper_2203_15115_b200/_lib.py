@@ -29,8 +29,9 @@ class CoarseND(ctypes.Structure):
         ("d_G", P), ("d_Gt", P), ("d_Z", P),
         ("d_sdof", P), ("d_udof", P), ("d_fS", P), ("d_cU", P),
         ("d_fwd_items", P), ("d_bwd_items", P),
-        ("h_fwd_ptr", P), ("h_bwd_ptr", P), ("d_phase_done", P),
+        ("h_fwd_ptr", P), ("h_bwd_ptr", P),
         ("d_factor", P), ("factor_bytes", c_size_t),
+        ("h_split", P), ("d_asm_nodes", P), ("h_asm_ptr", P), ("max_sep", c_int),
     ]
 
 

@@ -37,6 +37,9 @@ from ._lib import check, lib, ptr, stream_ptr
 
 log = logging.getLogger(__name__)
 
+#: fronts larger than this (DOFs) get a separate assembly pass in the forward solve
+SPLIT_FRONT = int(__import__("os").environ.get("TVB_ND_SPLIT_FRONT", "2048"))
+
 
 @dataclass
 class NDNode:
@@ -231,27 +234,43 @@ class NDCoarseSolver:
         # per-node scratch: f_S (s) and c_U (u); offsets sd_off / ud_off
         self.fS = torch.zeros(int(sd_off[-1]) + 1, dtype=torch.float64, device=dev)
         self.cU = torch.zeros(int(ud_off[-1]) + 1, dtype=torch.float64, device=dev)
-        # work items per height: (node, row0, row1); forward rows = u, backward rows = s
-        rows_per_item = 8
+        # work items per height: (node, row0, row1); forward rows = u, backward rows = s.
+        # 8 rows = one row per warp: longer chunks (to amortise the per-item
+        # front assembly) measured slower at C2(b), C4 and C5 (less parallelism).
+        def rows_per_item(front):
+            return 8
+
         fwd, bwd, fptr, bptr = [], [], [0], [0]
         heights = np.array([n.height for n in self.nodes])
         for h in range(self.height + 1):
             for ni in np.flatnonzero(heights == h):
-                nr = int(u[ni])
-                for r0 in range(0, max(nr, 1), rows_per_item):
-                    fwd.append((ni, r0, min(nr, r0 + rows_per_item)))
+                nr, step = int(u[ni]), rows_per_item(int(s[ni] + u[ni]))
+                for r0 in range(0, max(nr, 1), step):
+                    fwd.append((ni, r0, min(nr, r0 + step)))
             fptr.append(len(fwd))
         for h in range(self.height, -1, -1):
             for ni in np.flatnonzero(heights == h):
-                nr = int(s[ni])
-                for r0 in range(0, nr, rows_per_item):
-                    bwd.append((ni, r0, min(nr, r0 + rows_per_item)))
+                nr, step = int(s[ni]), rows_per_item(int(s[ni] + u[ni]))
+                for r0 in range(0, nr, step):
+                    bwd.append((ni, r0, min(nr, r0 + step)))
             bptr.append(len(bwd))
         self.fwd_items = torch.from_numpy(np.array(fwd, dtype=np.int32).reshape(-1, 3)).to(dev)
         self.bwd_items = torch.from_numpy(np.array(bwd, dtype=np.int32).reshape(-1, 3)).to(dev)
         self.fwd_ptr = np.array(fptr, dtype=np.int64)
         self.bwd_ptr = np.array(bptr, dtype=np.int64)
         self.max_front = int((s + u).max())
+        self.max_sep = int(s.max())
+        # heights whose largest front exceeds SPLIT_FRONT use a separate
+        # per-node assembly launch (the fused item would re-assemble the whole
+        # front for every 8-row chunk)
+        self.split = np.array([int(max(int(s[i] + u[i]) for i in np.flatnonzero(heights == h)) > SPLIT_FRONT)
+                               for h in range(self.height + 1)], dtype=np.int32)
+        asm, aptr = [], [0]
+        for h in range(self.height + 1):
+            asm.extend(np.flatnonzero(heights == h).tolist())
+            aptr.append(len(asm))
+        self.asm_nodes = torch.from_numpy(np.array(asm, dtype=np.int32)).to(dev)
+        self.asm_ptr = np.array(aptr, dtype=np.int64)
         self.bytes = self.factor.numel() * 8
         self.desc = self._make_desc() if self._make else None
 
@@ -272,13 +291,12 @@ class NDCoarseSolver:
         self._bptr = (ctypes.c_longlong * len(self.bwd_ptr))(*self.bwd_ptr.tolist())
         d.h_fwd_ptr = ctypes.cast(self._fptr, ctypes.c_void_p)
         d.h_bwd_ptr = ctypes.cast(self._bptr, ctypes.c_void_p)
-        import os
-
-        import torch
-
-        if os.environ.get("TVB_ND_PERSISTENT", "0") == "1" and 2 * (self.height + 1) <= 63:
-            self.phase_done = torch.zeros(2 * (self.height + 1), dtype=torch.int32, device=self.G.device)
-            d.d_phase_done = ptr(self.phase_done)
+        self._split = (ctypes.c_int * len(self.split))(*self.split.tolist())
+        self._aptr = (ctypes.c_longlong * len(self.asm_ptr))(*self.asm_ptr.tolist())
+        d.h_split = ctypes.cast(self._split, ctypes.c_void_p)
+        d.d_asm_nodes = ptr(self.asm_nodes)
+        d.h_asm_ptr = ctypes.cast(self._aptr, ctypes.c_void_p)
+        d.max_sep = self.max_sep
         return d
 
     def solve_device(self, y, x):

@@ -109,23 +109,10 @@ static CoarseNDDev coarse_nd_dev(const tvb_coarse_nd* d) {
   D.bwd_items = d->d_bwd_items;
   D.fwd_ptr = d->h_fwd_ptr;
   D.bwd_ptr = d->h_bwd_ptr;
-  D.phases = CoarsePhases{};
-  const int nph = 2 * (d->height + 1);
-  if (d->d_phase_done != nullptr && nph <= 63) {
-    D.phases.n_phases = nph;
-    D.phases.last_fwd = d->height;
-    D.phases.done = d->d_phase_done;
-    long long acc = 0;
-    for (int h = 0; h <= d->height; ++h) {
-      D.phases.start[h] = acc;
-      acc += d->h_fwd_ptr[h + 1] - d->h_fwd_ptr[h];
-    }
-    for (int h = 0; h <= d->height; ++h) {
-      D.phases.start[d->height + 1 + h] = acc;
-      acc += d->h_bwd_ptr[h + 1] - d->h_bwd_ptr[h];
-    }
-    D.phases.start[nph] = acc;
-  }
+  D.split = d->h_split;
+  D.asm_nodes = d->d_asm_nodes;
+  D.asm_ptr = d->h_asm_ptr;
+  D.max_sep = d->max_sep;
   return D;
 }
 

@@ -3,15 +3,6 @@
 
 namespace tvb {
 
-// Phase table of the persistent solve: phases 0..last_fwd are the forward
-// heights, the rest the backward heights; start[p] = first item of phase p in
-// the concatenated (fwd items, bwd items) list; done[p] device counters.
-struct CoarsePhases {
-  int n_phases, last_fwd;
-  long long start[64];
-  unsigned* done;
-};
-
 // Device view of the nested-dissection coarse factor (see coarse.py /
 // tvb_coarse_nd in include/topovox_b200.h).
 struct CoarseNDDev {
@@ -30,7 +21,10 @@ struct CoarseNDDev {
   const int* bwd_items;       // [n][3], grouped by height (root first)
   const long long* fwd_ptr;   // host: height+2 group offsets
   const long long* bwd_ptr;   // host
-  CoarsePhases phases;        // persistent-kernel schedule (done == nullptr: per-height launches)
+  const int* split;           // host, per height: 1 = separate assembly pass (large fronts)
+  const int* asm_nodes;       // device: nodes grouped by height (assembly pass)
+  const long long* asm_ptr;   // host: height+2 offsets into asm_nodes
+  int max_sep;                // largest separator (smem of the row pass)
 };
 
 cudaError_t launch_coarse_nd(const CoarseNDDev& D, const double* y, double* x, const int* stop, cudaStream_t s);
