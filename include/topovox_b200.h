@@ -63,6 +63,11 @@ int tvb_matvec(int nx, int ny, int nz, const double* h_mh45, const double* d_u, 
  * out7 = {threads, wx, wy, tiles_x, tiles_y, persistent CTAs, 0} */
 int tvb_matvec_plan(int nx, int ny, int nz, int* h_out7);
 
+/* diagnostics: sustained fp64 FMA throughput of this GPU measured live
+ * (independent DFMA chains on every SM), in TFLOP/s (2 flops per FMA);
+ * the denominator of the north-star fp64 roofline. Synchronous. */
+double tvb_fp64_peak_tflops(void* stream);
+
 /* apply_block24_subset (numba_kernels.py:31-46): out += K_subset u using only
  * the listed elements (duplicates count with multiplicity). d_ws: f64[Ne] + i32[Ne]. */
 int tvb_matvec_subset(int nx, int ny, int nz, const double* h_mh45, const double* d_u, double* d_out,

@@ -69,6 +69,20 @@ __global__ void k_masked_copy(long long nn, const double* u, const uint8_t* nfla
   out[i] = ((nflags[i / 3] >> (i % 3)) & 1) ? 0.0 : u[i];
 }
 
+// fp64 pipe probe: 8 independent DFMA chains per thread, 8 CTAs of 256 per SM
+__global__ void k_fp64_probe(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a, b);
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 12345.678) out[0] = s;
+}
+
 __global__ void k_sum_partials(const double* partials, int n, double* out) {
   __shared__ double red[32];
   double s = 0.0;
@@ -222,6 +236,33 @@ int tvb_matvec(int nx, int ny, int nz, const double* h_mh45, const double* d_u, 
   if (st || !d_dot) return st;
   k_sum_partials<<<1, 256, 0, s>>>((const double*)d_ws, pl.nblocks(), d_dot);
   return check(cudaGetLastError());
+}
+
+double tvb_fp64_peak_tflops(void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  double* sink = nullptr;
+  if (cudaMalloc(&sink, sizeof(double)) != cudaSuccess) return 0.0;
+  const dim3 grid(num_sms() * 8), block(256);
+  const int iters = 4096;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k_fp64_probe<<<grid, block, 0, s>>>(sink, 64, 1.0000001, 1e-9);  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(e0, s);
+    k_fp64_probe<<<grid, block, 0, s>>>(sink, iters, 1.0000001, 1e-9);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms > 0.f && ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  const double fmas = (double)grid.x * block.x * iters * 8.0;
+  return 2.0 * fmas / (best * 1e-3) / 1e12;
 }
 
 int tvb_matvec_plan(int nx, int ny, int nz, int* out7) {
