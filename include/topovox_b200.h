@@ -121,30 +121,38 @@ int tvb_coarse_dense(int nx, int ny, int nz, int block, const double* d_Es, doub
 /* a7: exact coarse solve x = E^-1 y with the nested-dissection block-LDL^T
  * factor (paper_2203_15115_b200/coarse.py builds it). Replaces the dense
  * cho_solve of DeflationSpace.coarse_solve (fea.py:208-211). All d_* are
- * device arrays described in coarse.py; h_fwd_ptr / h_bwd_ptr are host
- * arrays of height+2 work-item group offsets. */
+ * device arrays described in coarse.py; h_* are host arrays. Coarse vectors
+ * of tvb_coarse_nd_solve are in ND order (natural block B at ND block
+ * d_perm[B]); tvb_pcg_solve applies d_perm inside restriction/prolongation. */
 typedef struct tvb_coarse_nd {
-  int n_nodes, height, max_front;
-  const long long* d_meta;
+  int n_levels;             /* bottom tree heights factored node by node */
+  int max_front, max_sep;
+  const long long* d_meta;  /* [bottom node][8] s,u,g_off,z_off,sd_off,ud_off,child_begin,child_end */
   const long long* d_children;
   const int* d_cmap;
   const double* d_G;
   const double* d_Gt;
   const double* d_Z;
-  const int* d_sdof;
   const int* d_udof;
   double* d_fS;
   double* d_cU;
   const int* d_fwd_items;
   const int* d_bwd_items;
-  const long long* h_fwd_ptr;
+  const long long* h_fwd_ptr;  /* n_levels+1 work-item group offsets */
   const long long* h_bwd_ptr;
-  const double* d_factor;   /* the single allocation holding G, G^T and Z (L2 persistence window) */
-  size_t factor_bytes;
   const int* h_split;       /* per height: 1 = separate front-assembly launch (large fronts) */
   const int* d_asm_nodes;   /* nodes grouped by height */
   const long long* h_asm_ptr;
-  int max_sep;
+  int n_top;                /* dense top set (heights >= n_levels), DOFs */
+  long long top_off;        /* its ND DOF offset (= 6 Nb - n_top) */
+  const double* d_ZT;       /* n_top x n_top inverse of the top Schur complement */
+  double* d_fT;
+  int n_tchildren;
+  const long long* d_tchildren;
+  const int* d_tmap;
+  const int* d_perm;        /* i32[Nb]: natural block -> ND block */
+  const double* d_factor;   /* the single allocation holding G, G^T, Z, ZT (L2 persistence window) */
+  size_t factor_bytes;
 } tvb_coarse_nd;
 int tvb_coarse_nd_solve(const tvb_coarse_nd* nd, const double* d_y, double* d_x, void* stream);
 

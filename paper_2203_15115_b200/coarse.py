@@ -9,17 +9,22 @@ so it is factored here by geometric nested dissection:
 * symbolic (host, once per block grid): recursive bisection of the block box
   along its longest axis by one-block-thick separator planes down to small
   leaf boxes; for each tree node its separator S and update set U (the
-  ancestor-separator blocks adjacent to the node's box);
-* numeric (device, once per operator): multifrontal block-LDL^T. For each node
-  in postorder the front F = [[F_SS, F_SU], [F_US, F_UU]] is assembled from the
-  stencil and the children's update matrices, then
-      Z = F_SS^-1,  G = F_US Z,  update = F_UU - G F_SU  (passed to the parent);
+  ancestor-separator blocks adjacent to the node's box). Coarse DOFs are
+  renumbered in ND order (separators by increasing tree height), so every
+  separator is a contiguous DOF range and the top levels form the tail.
+* numeric (device, once per operator): multifrontal block LDL^T for the
+  "bottom" nodes (height < H0): per node, in order of height,
+      Z = F_SS^-1,  G = F_US Z,  update = F_UU - G F_SU  (to the parent front);
+  the "top" nodes (height >= H0, at most TOP_MAX DOFs in total) are not
+  factored node by node: their Schur complement S_T (original entries among
+  top DOFs plus the updates of the bottom nodes whose parent is a top node) is
+  inverted densely. H0 = 0 gives a pure dense inverse (small coarse spaces).
 * solve (device, every CG iteration, hand-written kernels in coarse.cu):
-      forward, leaves -> root:  f_S = y_S + sum(children), c_U = f_U - G f_S
-      backward, root -> leaves: x_S = Z f_S - G^T x_U
-  i.e. exactly one kernel per tree height and direction, reading G, G^T and Z
-  once each. The exact coarse solve keeps the DPCG iterates identical (up to
-  rounding) to the reference's dense Cholesky.
+      forward, bottom heights 0..H0-1:  f_S = y_S + sum(children c|S), c_U = f_U - G f_S
+      top:                              x_T = S_T^-1 (y_T + sum(children c|T))
+      backward, heights H0-1..0:        x_S = Z f_S - G^T x_U
+  The exact coarse solve keeps the DPCG iterates identical (up to rounding) to
+  the reference's dense Cholesky.
 
 The dense per-front linear algebra of the factorisation uses torch on the
 device (cuSOLVER/cuBLAS); it runs once per topology, not per iteration.
@@ -29,6 +34,7 @@ from __future__ import annotations
 
 import ctypes
 import logging
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -38,7 +44,10 @@ from ._lib import check, lib, ptr, stream_ptr
 log = logging.getLogger(__name__)
 
 #: fronts larger than this (DOFs) get a separate assembly pass in the forward solve
-SPLIT_FRONT = int(__import__("os").environ.get("TVB_ND_SPLIT_FRONT", "2048"))
+SPLIT_FRONT = int(os.environ.get("TVB_ND_SPLIT_FRONT", "2048"))
+#: largest top set inverted densely (DOFs); the top tree levels it replaces
+#: would otherwise cost two latency-bound launches each
+TOP_MAX = int(os.environ.get("TVB_ND_TOP_MAX", "4608"))
 
 
 @dataclass
@@ -48,6 +57,7 @@ class NDNode:
     children: list = field(default_factory=list)
     height: int = 0
     box: tuple = ()
+    parent: int = -1
 
 
 def nested_dissection(mx: int, my: int, mz: int, leaf_max: int = 27) -> list[NDNode]:
@@ -90,203 +100,255 @@ def nested_dissection(mx: int, my: int, mz: int, leaf_max: int = 27) -> list[NDN
             node.children = kids
             node.height = 1 + max(nodes[k].height for k in kids) if kids else 0
         nodes.append(node)
-        return len(nodes) - 1
+        me = len(nodes) - 1
+        for k in node.children:
+            nodes[k].parent = me
+        return me
 
     rec((0, mx, 0, my, 0, mz), np.empty(0, dtype=np.int64))
     return nodes
 
 
-class NDCoarseSolver:
-    """Factor E (block stencil Es on the device) and hold the device data of
-    the per-iteration solve kernels (see ``tvb_coarse_nd_*`` in the C-ABI)."""
+def _dofs(first_block_pos: np.ndarray) -> np.ndarray:
+    return (6 * first_block_pos[:, None] + np.arange(6)[None, :]).ravel()
 
-    def __init__(self, grid: tuple[int, int, int], Es, leaf_max: int = 27, make_desc: bool = True):
+
+class NDCoarseSolver:
+    """Factor E (block stencil ``Es`` on the device, natural block order) and
+    hold the device data of the per-iteration solve (``tvb_coarse_nd_solve``).
+    Solve vectors are in ND order: natural block B sits at ND block ``perm[B]``."""
+
+    def __init__(self, grid: tuple[int, int, int], Es, leaf_max: int = 27, top_max: int | None = None,
+                 make_desc: bool = True):
         import torch
 
         mx, my, mz = grid
         self.grid = grid
-        self.nb = mx * my * mz
-        self.nodes = nested_dissection(mx, my, mz, leaf_max)
-        nodes = self.nodes
-        self.height = max(n.height for n in nodes)
-        # ---- host index structures ------------------------------------
-        s_blocks = [n.sep.size for n in nodes]
-        u_blocks = [n.upd.size for n in nodes]
-        s = np.array(s_blocks, dtype=np.int64) * 6
-        u = np.array(u_blocks, dtype=np.int64) * 6
-        self.s, self.u = s, u
-
-        def dofs(blocks):
-            return (6 * blocks[:, None] + np.arange(6)[None, :]).ravel().astype(np.int32)
-
-        s_dof = [dofs(n.sep) for n in nodes]
-        u_dof = [dofs(n.upd) for n in nodes]
-        # child maps: child's U position -> parent's front position
-        cmaps = []
-        child_ptr = [0]
-        child_list = []
+        self.nb = nb = mx * my * mz
+        nodes = nested_dissection(mx, my, mz, leaf_max)
+        self.nodes = nodes
+        H = max(n.height for n in nodes)
+        top_max = TOP_MAX if top_max is None else top_max
+        seps_by_h = np.zeros(H + 2, dtype=np.int64)
         for n in nodes:
-            pos = {int(b): i for i, b in enumerate(np.concatenate([n.sep, n.upd]))}
-            for c in n.children:
-                cb = nodes[c].upd
-                m = np.array([pos[int(b)] for b in cb], dtype=np.int64)
-                cmaps.append((6 * m[:, None] + np.arange(6)[None, :]).ravel().astype(np.int32))
-                child_list.append(c)
-            child_ptr.append(len(child_list))
+            seps_by_h[n.height] += 6 * n.sep.size
+        tail = np.cumsum(seps_by_h[::-1])[::-1]  # DOFs at heights >= h
+        self.H0 = next(h for h in range(H + 2) if tail[h] <= top_max)
+        order = sorted(range(len(nodes)), key=lambda i: (nodes[i].height, i))
+        bottom = [i for i in order if nodes[i].height < self.H0]
+        top = [i for i in order if nodes[i].height >= self.H0]
+        self.n_bottom_levels = self.H0
+        # ND block order: bottom separators by height, then the top set
+        blk_order = np.concatenate([nodes[i].sep for i in bottom + top]).astype(np.int64)
+        perm = np.empty(nb, dtype=np.int64)
+        perm[blk_order] = np.arange(nb)
+        self.perm_host = perm
+        self.n_top = 6 * int(sum(nodes[i].sep.size for i in top))
+        self.top_off = 6 * nb - self.n_top
+        bidx = {ni: k for k, ni in enumerate(bottom)}
+        self._factor(torch, Es, nodes, bottom, top, bidx, perm)
         self._make = make_desc
-        self._factor(torch, Es, nodes, s, u, s_dof, u_dof, cmaps, child_ptr, child_list)
+        self.desc = self._make_desc() if make_desc else None
 
     # ------------------------------------------------------------------
-    def _factor(self, torch, Es, nodes, s, u, s_dof, u_dof, cmaps, child_ptr, child_list):
+    def _stencil_entries(self, rows_blocks, pos):
+        """(row pos, col pos, source block, neighbour slot) of the original E
+        entries with the row in ``rows_blocks`` and the column at pos >= 0."""
         mx, my, mz = self.grid
+        sb = rows_blocks
+        x, y, z = sb % mx, (sb // mx) % my, sb // (mx * my)
+        out = [[], [], [], []]
+        for d in range(27):
+            cx, cy, cz = x + d % 3 - 1, y + (d // 3) % 3 - 1, z + d // 9 - 1
+            ok = (cx >= 0) & (cx < mx) & (cy >= 0) & (cy < my) & (cz >= 0) & (cz < mz)
+            cb = np.where(ok, cx + mx * (cy + my * cz), 0)
+            pc = np.where(ok, pos[cb], -1)
+            keep = ok & (pc >= 0)
+            out[0].append(np.arange(sb.size)[keep])
+            out[1].append(pc[keep])
+            out[2].append(sb[keep])
+            out[3].append(np.full(int(keep.sum()), d))
+        return [np.concatenate(o) for o in out]
+
+    def _scatter_blocks(self, torch, F, E6, rows, cols, srcB, srcD, mirror_from):
+        dev = F.device
+        blk = E6[torch.from_numpy(srcB).to(dev), torch.from_numpy(srcD).to(dev)]
+        ar = torch.arange(6, device=dev)
+        r6 = torch.from_numpy(6 * rows).to(dev)[:, None, None] + ar[None, :, None]
+        c6 = torch.from_numpy(6 * cols).to(dev)[:, None, None] + ar[None, None, :]
+        F[r6.expand(-1, 6, 6), c6.expand(-1, 6, 6)] = blk
+        if mirror_from is not None:
+            m = cols >= mirror_from
+            if m.any():
+                mt = torch.from_numpy(m).to(dev)
+                F[c6[mt].expand(-1, 6, 6).transpose(1, 2), r6[mt].expand(-1, 6, 6).transpose(1, 2)] = \
+                    blk[mt].transpose(1, 2)
+
+    def _factor(self, torch, Es, nodes, bottom, top, bidx, perm):
         dev = Es.device
-        E6 = Es.view(self.nb, 27, 6, 6)
-        upd_mats = {}
+        nb = self.nb
+        E6 = Es.view(nb, 27, 6, 6)
+        upd = {}
         G_list, Z_list = [], []
-        cm_iter = 0
-        for ni, n in enumerate(nodes):
-            blocks = np.concatenate([n.sep, n.upd])
+        s_list, u_list, sd_list, udof_list, cmaps, children = [], [], [], [], [], []
+        child_ptr = [0]
+        blk_cursor = 0
+        for ni in bottom:
+            n = nodes[ni]
             ns, nu = n.sep.size, n.upd.size
-            f = 6 * (ns + nu)
-            F = torch.zeros((f, f), dtype=torch.float64, device=dev)
-            # original entries E[S, S u U]: neighbour offsets of every separator block
-            pos = -np.ones(self.nb, dtype=np.int64)
-            pos[blocks] = np.arange(blocks.size)
-            sb = n.sep
-            x, y, z = sb % mx, (sb // mx) % my, sb // (mx * my)
-            rows, cols, srcB, srcD = [], [], [], []
-            for d in range(27):
-                dx, dy, dz = d % 3 - 1, (d // 3) % 3 - 1, d // 9 - 1
-                cx, cy, cz = x + dx, y + dy, z + dz
-                ok = (cx >= 0) & (cx < mx) & (cy >= 0) & (cy < my) & (cz >= 0) & (cz < mz)
-                cb = cx + mx * (cy + my * cz)
-                pc = np.where(ok, pos[np.where(ok, cb, 0)], -1)
-                keep = ok & (pc >= 0)
-                rows.append(np.arange(ns)[keep])
-                cols.append(pc[keep])
-                srcB.append(sb[keep])
-                srcD.append(np.full(int(keep.sum()), d))
-            rows, cols = np.concatenate(rows), np.concatenate(cols)
-            srcB, srcD = np.concatenate(srcB), np.concatenate(srcD)
-            blk = E6[torch.from_numpy(srcB).to(dev), torch.from_numpy(srcD).to(dev)]  # (k, 6, 6)
-            r6 = torch.from_numpy(6 * rows).to(dev)[:, None, None] + torch.arange(6, device=dev)[None, :, None]
-            c6 = torch.from_numpy(6 * cols).to(dev)[:, None, None] + torch.arange(6, device=dev)[None, None, :]
-            F[r6.expand(-1, 6, 6), c6.expand(-1, 6, 6)] = blk
-            # U x S part = transpose of S x U (entries with a column in U)
-            inU = cols >= ns
-            if inU.any():
-                F[c6[inU].expand(-1, 6, 6).transpose(1, 2), r6[inU].expand(-1, 6, 6).transpose(1, 2)] = \
-                    blk[torch.from_numpy(inU).to(dev)].transpose(1, 2)
-            # extend-add children's update matrices (fixed order: deterministic)
+            front = np.concatenate([n.sep, n.upd])
+            pos = -np.ones(nb, dtype=np.int64)
+            pos[front] = np.arange(front.size)
+            F = torch.zeros((6 * front.size, 6 * front.size), dtype=torch.float64, device=dev)
+            rows, cols, srcB, srcD = self._stencil_entries(n.sep, pos)
+            self._scatter_blocks(torch, F, E6, rows, cols, srcB, srcD, mirror_from=ns)
             for c in n.children:
-                m = torch.from_numpy(cmaps[cm_iter].astype(np.int64)).to(dev)
-                cm_iter += 1
-                Uc = upd_mats.pop(c)
-                F[m[:, None], m[None, :]] += Uc
+                m = _dofs(pos[nodes[c].upd])
+                Uc = upd.pop(c)
+                mt = torch.from_numpy(m).to(dev)
+                F[mt[:, None], mt[None, :]] += Uc
+                cmaps.append(m.astype(np.int32))
+                children.append(bidx[c])
+            child_ptr.append(len(children))
             S = 6 * ns
-            Fss = 0.5 * (F[:S, :S] + F[:S, :S].T)
-            L, info = torch.linalg.cholesky_ex(Fss)
+            L, info = torch.linalg.cholesky_ex(0.5 * (F[:S, :S] + F[:S, :S].T))
             if int(info.item()) != 0:
                 raise np.linalg.LinAlgError(f"coarse front {ni} not SPD")
             Z = torch.cholesky_inverse(L)
             G = F[S:, :S] @ Z
             if nu:
-                upd_mats[ni] = F[S:, S:] - G @ F[:S, S:]
+                upd[ni] = F[S:, S:] - G @ F[:S, S:]
             Z_list.append(Z.contiguous())
             G_list.append(G.contiguous())
+            s_list.append(S)
+            u_list.append(6 * nu)
+            sd_list.append(6 * blk_cursor)
+            blk_cursor += ns
+            udof_list.append(_dofs(perm[n.upd]).astype(np.int32))
             del F
-        self._pack(torch, dev, G_list, Z_list, s, u, s_dof, u_dof, cmaps, child_ptr, child_list)
+        # ---- dense top: S_T = E_TT + updates of bottom nodes with a top parent
+        self.Ztop = None
+        tchildren, tmaps = [], []
+        if self.n_top:
+            tblocks = np.concatenate([nodes[i].sep for i in top]).astype(np.int64)
+            tpos = -np.ones(nb, dtype=np.int64)
+            tpos[tblocks] = perm[tblocks] - (nb - tblocks.size)
+            ST = torch.zeros((self.n_top, self.n_top), dtype=torch.float64, device=dev)
+            rows, cols, srcB, srcD = self._stencil_entries(tblocks, tpos)
+            rows = tpos[srcB]
+            self._scatter_blocks(torch, ST, E6, rows, cols, srcB, srcD, mirror_from=None)
+            for ni in bottom:
+                if nodes[ni].parent >= 0 and nodes[nodes[ni].parent].height >= self.H0:
+                    m = _dofs(tpos[nodes[ni].upd])
+                    mt = torch.from_numpy(m).to(dev)
+                    ST[mt[:, None], mt[None, :]] += upd.pop(ni)
+                    tchildren.append(bidx[ni])
+                    tmaps.append(m.astype(np.int32))
+            L, info = torch.linalg.cholesky_ex(0.5 * (ST + ST.T))
+            if int(info.item()) != 0:
+                raise np.linalg.LinAlgError("coarse top Schur complement not SPD")
+            self.Ztop = torch.cholesky_inverse(L).contiguous()
+            del ST, L
+        assert not upd, "unconsumed update matrices"
+        self._pack(torch, dev, G_list, Z_list, np.array(s_list, np.int64), np.array(u_list, np.int64),
+                   np.array(sd_list, np.int64), udof_list, cmaps, child_ptr, children, tchildren, tmaps,
+                   [nodes[i].height for i in bottom])
 
-    def _pack(self, torch, dev, G_list, Z_list, s, u, s_dof, u_dof, cmaps, child_ptr, child_list):
-        nn = len(self.nodes)
-        g_off = np.zeros(nn + 1, dtype=np.int64)
-        z_off = np.zeros(nn + 1, dtype=np.int64)
-        g_off[1:] = np.cumsum(s * u)
-        z_off[1:] = np.cumsum(s * s)
-        # G, G^T and Z live in ONE allocation so the solver can pin it in L2
-        # with a single access-policy window (tvb_pcg_solve, coarse_kind 1).
+    def _pack(self, torch, dev, G_list, Z_list, s, u, sd, udof_list, cmaps, child_ptr, children, tchildren,
+              tmaps, heights):
+        nbot = len(G_list)
+        self.n_bottom = nbot
+        self.s, self.u = s, u
+        g_off = np.zeros(nbot + 1, dtype=np.int64)
+        z_off = np.zeros(nbot + 1, dtype=np.int64)
+        if nbot:
+            g_off[1:] = np.cumsum(s * u)
+            z_off[1:] = np.cumsum(s * s)
         ng, nz = int(g_off[-1]), int(z_off[-1])
-        self.factor = torch.empty(2 * ng + nz + 2, dtype=torch.float64, device=dev)
+        ntop2 = self.n_top * self.n_top
+        # G, G^T, Z and the dense top inverse in ONE allocation
+        self.factor = torch.zeros(2 * ng + nz + ntop2 + 4, dtype=torch.float64, device=dev)
         self.G = self.factor[:ng + 1]
         self.Gt = self.factor[ng + 1:2 * ng + 2]
-        self.Z = self.factor[2 * ng + 2:]
+        self.Z = self.factor[2 * ng + 2:2 * ng + nz + 3]
+        self.ZT = self.factor[2 * ng + nz + 3:]
         if ng:
             self.G[:ng] = torch.cat([g.reshape(-1) for g in G_list])
             self.Gt[:ng] = torch.cat([g.T.contiguous().reshape(-1) for g in G_list])
-        self.Z[:] = torch.cat([z.reshape(-1) for z in Z_list])
-        sd_off = np.zeros(nn + 1, dtype=np.int64)
-        ud_off = np.zeros(nn + 1, dtype=np.int64)
-        sd_off[1:] = np.cumsum(s)
-        ud_off[1:] = np.cumsum(u)
-        self.s_dof = torch.from_numpy(np.concatenate(s_dof)).to(dev)
-        self.u_dof = torch.from_numpy(np.concatenate(u_dof + [np.zeros(1, np.int32)])).to(dev)
+        if nz:
+            self.Z[:nz] = torch.cat([z.reshape(-1) for z in Z_list])
+        if ntop2:
+            self.ZT[:ntop2] = self.Ztop.reshape(-1)
+        self.Ztop = None
+        ud_off = np.zeros(nbot + 1, dtype=np.int64)
+        if nbot:
+            ud_off[1:] = np.cumsum(u)
+        self.udof = torch.from_numpy(np.concatenate(udof_list + [np.zeros(1, np.int32)])).to(dev)
         cm_off = np.zeros(len(cmaps) + 1, dtype=np.int64)
         cm_off[1:] = np.cumsum([c.size for c in cmaps])
         self.cmap = torch.from_numpy(np.concatenate(cmaps + [np.zeros(1, np.int32)])).to(dev)
-        # per-node meta (int64): s, u, g_off, z_off, sd_off, ud_off, child_begin, child_end
-        meta = np.stack([s, u, g_off[:-1], z_off[:-1], sd_off[:-1], ud_off[:-1],
-                         np.array(child_ptr[:-1]), np.array(child_ptr[1:])], axis=1).astype(np.int64)
+        meta = np.zeros((max(nbot, 1), 8), dtype=np.int64)
+        if nbot:
+            meta[:] = np.stack([s, u, g_off[:-1], z_off[:-1], sd, ud_off[:-1], np.array(child_ptr[:-1]),
+                                np.array(child_ptr[1:])], axis=1)
         self.meta = torch.from_numpy(np.ascontiguousarray(meta)).to(dev)
-        # child list entries: (child node, cmap offset)
-        ch = np.stack([np.array(child_list, dtype=np.int64), cm_off[:-1]], axis=1) if child_list else \
+        ch = np.stack([np.array(children, dtype=np.int64), cm_off[:-1]], axis=1) if children else \
             np.zeros((1, 2), dtype=np.int64)
         self.children = torch.from_numpy(np.ascontiguousarray(ch)).to(dev)
-        # per-node scratch: f_S (s) and c_U (u); offsets sd_off / ud_off
-        self.fS = torch.zeros(int(sd_off[-1]) + 1, dtype=torch.float64, device=dev)
+        tm_off = np.zeros(len(tmaps) + 1, dtype=np.int64)
+        tm_off[1:] = np.cumsum([t.size for t in tmaps])
+        self.tmap = torch.from_numpy(np.concatenate(tmaps + [np.zeros(1, np.int32)])).to(dev)
+        tch = np.stack([np.array(tchildren, dtype=np.int64), tm_off[:-1]], axis=1) if tchildren else \
+            np.zeros((1, 2), dtype=np.int64)
+        self.tchildren = torch.from_numpy(np.ascontiguousarray(tch)).to(dev)
+        self.n_tchildren = len(tchildren)
+        n_c = 6 * self.nb
+        self.fS = torch.zeros(n_c + 1, dtype=torch.float64, device=dev)   # indexed by ND dof
         self.cU = torch.zeros(int(ud_off[-1]) + 1, dtype=torch.float64, device=dev)
-        # work items per height: (node, row0, row1); forward rows = u, backward rows = s.
-        # 8 rows = one row per warp: longer chunks (to amortise the per-item
-        # front assembly) measured slower at C2(b), C4 and C5 (less parallelism).
-        def rows_per_item(front):
-            return 8
-
+        self.fT = torch.zeros(self.n_top + 1, dtype=torch.float64, device=dev)
+        self.perm = torch.from_numpy(self.perm_host.astype(np.int32)).to(dev)
+        # work items per bottom height: (node, row0, row1); fwd rows = u, bwd rows = s; 8 rows = 1 per warp
+        heights = np.array(heights, dtype=np.int64)
+        step = 8
         fwd, bwd, fptr, bptr = [], [], [0], [0]
-        heights = np.array([n.height for n in self.nodes])
-        for h in range(self.height + 1):
+        for h in range(self.H0):
             for ni in np.flatnonzero(heights == h):
-                nr, step = int(u[ni]), rows_per_item(int(s[ni] + u[ni]))
+                nr = int(u[ni])
                 for r0 in range(0, max(nr, 1), step):
                     fwd.append((ni, r0, min(nr, r0 + step)))
             fptr.append(len(fwd))
-        for h in range(self.height, -1, -1):
+        for h in range(self.H0 - 1, -1, -1):
             for ni in np.flatnonzero(heights == h):
-                nr, step = int(s[ni]), rows_per_item(int(s[ni] + u[ni]))
+                nr = int(s[ni])
                 for r0 in range(0, nr, step):
                     bwd.append((ni, r0, min(nr, r0 + step)))
             bptr.append(len(bwd))
-        self.fwd_items = torch.from_numpy(np.array(fwd, dtype=np.int32).reshape(-1, 3)).to(dev)
-        self.bwd_items = torch.from_numpy(np.array(bwd, dtype=np.int32).reshape(-1, 3)).to(dev)
+        self.fwd_items = torch.from_numpy(np.array(fwd or [(0, 0, 0)], dtype=np.int32).reshape(-1, 3)).to(dev)
+        self.bwd_items = torch.from_numpy(np.array(bwd or [(0, 0, 0)], dtype=np.int32).reshape(-1, 3)).to(dev)
         self.fwd_ptr = np.array(fptr, dtype=np.int64)
         self.bwd_ptr = np.array(bptr, dtype=np.int64)
-        self.max_front = int((s + u).max())
-        self.max_sep = int(s.max())
-        # heights whose largest front exceeds SPLIT_FRONT use a separate
-        # per-node assembly launch (the fused item would re-assemble the whole
-        # front for every 8-row chunk)
+        self.max_front = int((s + u).max()) if nbot else 1
+        self.max_sep = int(s.max()) if nbot else 1
         self.split = np.array([int(max(int(s[i] + u[i]) for i in np.flatnonzero(heights == h)) > SPLIT_FRONT)
-                               for h in range(self.height + 1)], dtype=np.int32)
+                               for h in range(self.H0)] or [0], dtype=np.int32)
         asm, aptr = [], [0]
-        for h in range(self.height + 1):
+        for h in range(self.H0):
             asm.extend(np.flatnonzero(heights == h).tolist())
             aptr.append(len(asm))
-        self.asm_nodes = torch.from_numpy(np.array(asm, dtype=np.int32)).to(dev)
+        self.asm_nodes = torch.from_numpy(np.array(asm or [0], dtype=np.int32)).to(dev)
         self.asm_ptr = np.array(aptr, dtype=np.int64)
         self.bytes = self.factor.numel() * 8
-        self.desc = self._make_desc() if self._make else None
 
     def _make_desc(self):
         from ._lib import CoarseND
 
         d = CoarseND()
-        d.n_nodes = len(self.nodes)
-        d.height = self.height
-        d.max_front = self.max_front
+        d.n_levels = self.H0
+        d.max_front, d.max_sep = self.max_front, self.max_sep
         d.d_meta, d.d_children, d.d_cmap = ptr(self.meta), ptr(self.children), ptr(self.cmap)
         d.d_G, d.d_Gt, d.d_Z = ptr(self.G), ptr(self.Gt), ptr(self.Z)
-        d.d_sdof, d.d_udof = ptr(self.s_dof), ptr(self.u_dof)
-        d.d_fS, d.d_cU = ptr(self.fS), ptr(self.cU)
+        d.d_udof, d.d_fS, d.d_cU = ptr(self.udof), ptr(self.fS), ptr(self.cU)
         d.d_fwd_items, d.d_bwd_items = ptr(self.fwd_items), ptr(self.bwd_items)
-        d.d_factor, d.factor_bytes = ptr(self.factor), self.bytes
         self._fptr = (ctypes.c_longlong * len(self.fwd_ptr))(*self.fwd_ptr.tolist())
         self._bptr = (ctypes.c_longlong * len(self.bwd_ptr))(*self.bwd_ptr.tolist())
         d.h_fwd_ptr = ctypes.cast(self._fptr, ctypes.c_void_p)
@@ -296,10 +358,18 @@ class NDCoarseSolver:
         d.h_split = ctypes.cast(self._split, ctypes.c_void_p)
         d.d_asm_nodes = ptr(self.asm_nodes)
         d.h_asm_ptr = ctypes.cast(self._aptr, ctypes.c_void_p)
-        d.max_sep = self.max_sep
+        d.n_top, d.top_off = self.n_top, self.top_off
+        d.d_ZT, d.d_fT = ptr(self.ZT), ptr(self.fT)
+        d.n_tchildren, d.d_tchildren, d.d_tmap = self.n_tchildren, ptr(self.tchildren), ptr(self.tmap)
+        d.d_perm = ptr(self.perm)
+        d.d_factor, d.factor_bytes = ptr(self.factor), self.bytes
         return d
 
     def solve_device(self, y, x):
-        """x = E^-1 y on device tensors (length 6 * n_blocks)."""
+        """x = E^-1 y on device tensors in ND order (length 6 * n_blocks)."""
         check(lib().tvb_coarse_nd_solve(ctypes.byref(self.desc), ptr(y), ptr(x), stream_ptr()), "coarse solve")
         return x
+
+    def nd_index(self):
+        """ND DOF position of every natural coarse DOF 6B + j (host array)."""
+        return _dofs(self.perm_host)

@@ -106,16 +106,15 @@ __global__ void k_subset_occ(long long ne, const int* counts, const double* occ,
 
 static CoarseNDDev coarse_nd_dev(const tvb_coarse_nd* d) {
   CoarseNDDev D;
-  D.n_nodes = d->n_nodes;
-  D.height = d->height;
+  D.n_levels = d->n_levels;
   D.max_front = d->max_front;
+  D.max_sep = d->max_sep;
   D.meta = d->d_meta;
   D.children = d->d_children;
   D.cmap = d->d_cmap;
   D.G = d->d_G;
   D.Gt = d->d_Gt;
   D.Z = d->d_Z;
-  D.sdof = d->d_sdof;
   D.udof = d->d_udof;
   D.fS = d->d_fS;
   D.cU = d->d_cU;
@@ -126,7 +125,14 @@ static CoarseNDDev coarse_nd_dev(const tvb_coarse_nd* d) {
   D.split = d->h_split;
   D.asm_nodes = d->d_asm_nodes;
   D.asm_ptr = d->h_asm_ptr;
-  D.max_sep = d->max_sep;
+  D.n_top = d->n_top;
+  D.top_off = d->top_off;
+  D.ZT = d->d_ZT;
+  D.fT = d->d_fT;
+  D.n_tchildren = d->n_tchildren;
+  D.tchildren = d->d_tchildren;
+  D.tmap = d->d_tmap;
+  D.perm = d->d_perm;
   return D;
 }
 

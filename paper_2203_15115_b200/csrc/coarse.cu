@@ -1,19 +1,19 @@
-// a7: per-iteration coarse solve E mu = y with the nested-dissection block
-// LDL^T factor built by paper_2203_15115_b200/coarse.py. Replaces the dense
+// a7: per-iteration coarse solve E mu = y with the nested-dissection factor
+// built by paper_2203_15115_b200/coarse.py. Replaces the dense
 // scipy.linalg.cho_solve of DeflationSpace.coarse_solve (topovox/fea.py:208-211).
+// Vectors are in ND order (every separator a contiguous DOF range).
 //
-// For every tree node N (separator S, update set U, front F = S u U):
-//   forward  (leaves -> root): f_S = y_S + sum_children c_child|S,
-//                              f_U =       sum_children c_child|U,
-//                              c_U = f_U - G f_S                (G = F_US F_SS^-1)
-//   backward (root -> leaves): x_S = Z f_S - G^T x_U            (Z = F_SS^-1)
-// One launch per tree height and direction (two for forward heights with
-// large fronts: a per-node assembly pass, then the rows); inside a launch,
+// Bottom tree node N (separator S, update set U, front F = S u U):
+//   forward  (heights 0..H0-1): f_S = y_S + sum_children c_child|S,
+//                               f_U =       sum_children c_child|U,
+//                               c_U = f_U - G f_S            (G = F_US F_SS^-1)
+//   backward (heights H0-1..0): x_S = Z f_S - G^T x_U         (Z = F_SS^-1)
+// Top set T (heights >= H0): x_T = S_T^-1 (y_T + sum_children c_child|T).
+// One launch per bottom height and direction (two for forward heights with
+// large fronts: a per-node assembly pass, then the rows) and two for the top;
 // work items are (node, 8-row chunk) pairs, one CTA each, one warp per matrix
-// row with a fixed-order lane-strided dot product + shuffle tree.
-// Children are extend-added in a fixed order, so the solve is bitwise
-// reproducible. Row-major G (forward) and G^T / Z (backward) make every
-// warp read contiguous rows.
+// row with a fixed-order lane-strided dot product + shuffle tree. Children are
+// extend-added in a fixed order: the solve is bitwise reproducible.
 #include "coarse.cuh"
 
 namespace tvb {
@@ -21,8 +21,7 @@ namespace tvb {
 constexpr int kCoarseThreads = 256;
 
 // Row . vector with the row streamed from global memory: 8 independent loads
-// in flight per lane (the row is not L1-resident; a dependent load chain
-// would cost a full memory latency per 32 elements). Fixed summation order.
+// in flight per lane. Fixed summation order.
 __device__ __forceinline__ double warp_dot(const double* __restrict__ a, const double* b, int n, int lane) {
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   int i = lane;
@@ -48,15 +47,8 @@ __device__ __forceinline__ double warp_dot(const double* __restrict__ a, const d
   return warp_sum((s0 + s1) + (s2 + s3));
 }
 
-// Fused forward item (small fronts): assemble the node's front vector in
-// shared memory, then c_U = f_U - G f_S for this item's rows.
-__device__ __forceinline__ void fwd_item(const CoarseNDDev& D, const int* it, const double* y, double* f) {
-  const int node = it[0], r0 = it[1], r1 = it[2];
-  const long long* m = D.meta + 8 * node;
-  const int s = (int)m[0], u = (int)m[1];
-  const long long g_off = m[2], sd_off = m[4], ud_off = m[5];
-  const int cb = (int)m[6], ce = (int)m[7];
-  for (int i = threadIdx.x; i < s + u; i += blockDim.x) f[i] = i < s ? y[D.sdof[sd_off + i]] : 0.0;
+// extend-add the children's update vectors into a front vector f (fixed order)
+__device__ __forceinline__ void add_children(const CoarseNDDev& D, int cb, int ce, double* f) {
   for (int k = cb; k < ce; ++k) {
     __syncthreads();
     const int cn = (int)D.children[2 * k];
@@ -67,6 +59,21 @@ __device__ __forceinline__ void fwd_item(const CoarseNDDev& D, const int* it, co
     for (int t = threadIdx.x; t < cu; t += blockDim.x) f[D.cmap[co + t]] += cc[t];
   }
   __syncthreads();
+}
+
+// Fused forward item (small fronts): assemble the front vector in shared
+// memory, then c_U = f_U - G f_S for this item's rows.
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_fwd(CoarseNDDev D, const int* items, const double* y,
+                                                               const int* stop) {
+  extern __shared__ double f[];
+  if (stop != nullptr && *stop) return;
+  const int* it = items + 3 * blockIdx.x;
+  const int node = it[0], r0 = it[1], r1 = it[2];
+  const long long* m = D.meta + 8 * node;
+  const int s = (int)m[0], u = (int)m[1];
+  const long long g_off = m[2], sd_off = m[4], ud_off = m[5];
+  for (int i = threadIdx.x; i < s + u; i += blockDim.x) f[i] = i < s ? y[sd_off + i] : 0.0;
+  add_children(D, (int)m[6], (int)m[7], f);
   if (r0 == 0)
     for (int i = threadIdx.x; i < s; i += blockDim.x) D.fS[sd_off + i] = f[i];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -76,8 +83,8 @@ __device__ __forceinline__ void fwd_item(const CoarseNDDev& D, const int* it, co
   }
 }
 
-// Split forward (large fronts), part 1: assemble f_S into fS and f_U into cU
-// of the node, once per node (children extend-added in fixed order).
+// Split forward (large fronts), part 1: assemble f_S into fS and f_U into cU,
+// once per node.
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_asm(CoarseNDDev D, const int* nodes, const double* y,
                                                                const int* stop) {
   if (stop != nullptr && *stop) return;
@@ -85,14 +92,13 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_asm(CoarseNDDev D, co
   const long long* m = D.meta + 8 * node;
   const int s = (int)m[0], u = (int)m[1];
   const long long sd_off = m[4], ud_off = m[5];
-  const int cb = (int)m[6], ce = (int)m[7];
   double* fS = D.fS + sd_off;
   double* fU = D.cU + ud_off;
   for (int i = threadIdx.x; i < s + u; i += blockDim.x) {
-    if (i < s) fS[i] = y[D.sdof[sd_off + i]];
+    if (i < s) fS[i] = y[sd_off + i];
     else fU[i - s] = 0.0;
   }
-  for (int k = cb; k < ce; ++k) {
+  for (int k = (int)m[6]; k < (int)m[7]; ++k) {
     __syncthreads();
     const int cn = (int)D.children[2 * k];
     const long long co = D.children[2 * k + 1];
@@ -125,7 +131,41 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_rows(CoarseNDDev D, c
   }
 }
 
-__device__ __forceinline__ void bwd_item(const CoarseNDDev& D, const int* it, double* x, double* sm) {
+// Top set, part 1: fT = y_T + children's update vectors (one CTA, fixed order).
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_top_asm(CoarseNDDev D, const double* y, const int* stop) {
+  if (stop != nullptr && *stop) return;
+  for (int i = threadIdx.x; i < D.n_top; i += blockDim.x) D.fT[i] = y[D.top_off + i];
+  for (int k = 0; k < D.n_tchildren; ++k) {
+    __syncthreads();
+    const int cn = (int)D.tchildren[2 * k];
+    const long long to = D.tchildren[2 * k + 1];
+    const long long* cm = D.meta + 8 * cn;
+    const int cu = (int)cm[1];
+    const double* cc = D.cU + cm[5];
+    for (int t = threadIdx.x; t < cu; t += blockDim.x) D.fT[D.tmap[to + t]] += cc[t];
+  }
+}
+
+// Top set, part 2: x_T = S_T^-1 fT (dense, one warp per row, 8 rows per CTA).
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_top_rows(CoarseNDDev D, double* x, const int* stop) {
+  extern __shared__ double ft[];
+  if (stop != nullptr && *stop) return;
+  const int n = D.n_top;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) ft[i] = D.fT[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int j = blockIdx.x * (kCoarseThreads / 32) + warp;
+  if (j < n) {
+    const double d = warp_dot(D.ZT + (long long)j * n, ft, n, lane);
+    if (lane == 0) x[D.top_off + j] = d;
+  }
+}
+
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_bwd(CoarseNDDev D, const int* items, double* x,
+                                                               const int* stop) {
+  extern __shared__ double sm[];
+  if (stop != nullptr && *stop) return;
+  const int* it = items + 3 * blockIdx.x;
   const int node = it[0], r0 = it[1], r1 = it[2];
   const long long* m = D.meta + 8 * node;
   const int s = (int)m[0], u = (int)m[1];
@@ -139,46 +179,41 @@ __device__ __forceinline__ void bwd_item(const CoarseNDDev& D, const int* it, do
   for (int j = r0 + warp; j < r1; j += nw) {
     const double a = warp_dot(D.Z + z_off + (long long)j * s, fs, s, lane);
     const double b = u ? warp_dot(D.Gt + g_off + (long long)j * u, xu, u, lane) : 0.0;
-    if (lane == 0) x[D.sdof[sd_off + j]] = a - b;
+    if (lane == 0) x[sd_off + j] = a - b;
   }
-}
-
-__global__ void __launch_bounds__(kCoarseThreads) k_coarse_fwd(CoarseNDDev D, const int* items, const double* y,
-                                                               const int* stop) {
-  extern __shared__ double sm[];
-  if (stop != nullptr && *stop) return;
-  fwd_item(D, items + 3 * blockIdx.x, y, sm);
-}
-
-__global__ void __launch_bounds__(kCoarseThreads) k_coarse_bwd(CoarseNDDev D, const int* items, double* x,
-                                                               const int* stop) {
-  extern __shared__ double sm[];
-  if (stop != nullptr && *stop) return;
-  bwd_item(D, items + 3 * blockIdx.x, x, sm);
 }
 
 cudaError_t launch_coarse_nd(const CoarseNDDev& D, const double* y, double* x, const int* stop, cudaStream_t s) {
   static int attr_max = 0;
   const int smem = (int)(sizeof(double) * (size_t)D.max_front);
-  if (smem > attr_max) {
-    cudaFuncSetAttribute(k_coarse_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k_coarse_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k_coarse_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_max = smem;
+  const int smem_top = (int)(sizeof(double) * (size_t)(D.n_top + 1));
+  const int smem_max = smem > smem_top ? smem : smem_top;
+  if (smem_max > attr_max) {
+    cudaFuncSetAttribute(k_coarse_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+    cudaFuncSetAttribute(k_coarse_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+    cudaFuncSetAttribute(k_coarse_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+    cudaFuncSetAttribute(k_coarse_top_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+    attr_max = smem_max;
   }
-  for (int h = 0; h <= D.height; ++h) {
+  for (int h = 0; h < D.n_levels; ++h) {
     const long long a = D.fwd_ptr[h], b = D.fwd_ptr[h + 1];
     if (b <= a) continue;
-    if (D.split != nullptr && D.split[h]) {
+    if (D.split[h]) {
       const long long na = D.asm_ptr[h], nb = D.asm_ptr[h + 1];
-      const int smem_rows = (int)(sizeof(double) * (size_t)D.max_sep);
       k_coarse_asm<<<(unsigned)(nb - na), kCoarseThreads, 0, s>>>(D, D.asm_nodes + na, y, stop);
-      k_coarse_rows<<<(unsigned)(b - a), kCoarseThreads, smem_rows, s>>>(D, D.fwd_items + 3 * a, stop);
+      k_coarse_rows<<<(unsigned)(b - a), kCoarseThreads, (int)(sizeof(double) * D.max_sep), s>>>(
+          D, D.fwd_items + 3 * a, stop);
     } else {
       k_coarse_fwd<<<(unsigned)(b - a), kCoarseThreads, smem, s>>>(D, D.fwd_items + 3 * a, y, stop);
     }
   }
-  for (int h = 0; h <= D.height; ++h) {  // bwd_ptr is ordered root level first
+  if (D.n_top > 0) {
+    k_coarse_top_asm<<<1, kCoarseThreads, 0, s>>>(D, y, stop);
+    const int rows_per_cta = kCoarseThreads / 32;
+    k_coarse_top_rows<<<(unsigned)((D.n_top + rows_per_cta - 1) / rows_per_cta), kCoarseThreads, smem_top, s>>>(
+        D, x, stop);
+  }
+  for (int h = 0; h < D.n_levels; ++h) {  // bwd_ptr groups are ordered top-most bottom level first
     const long long a = D.bwd_ptr[h], b = D.bwd_ptr[h + 1];
     if (b > a) k_coarse_bwd<<<(unsigned)(b - a), kCoarseThreads, smem, s>>>(D, D.bwd_items + 3 * a, x, stop);
   }

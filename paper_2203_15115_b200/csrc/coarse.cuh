@@ -3,28 +3,36 @@
 
 namespace tvb {
 
-// Device view of the nested-dissection coarse factor (see coarse.py /
-// tvb_coarse_nd in include/topovox_b200.h).
+// Device view of the nested-dissection coarse factor (built by coarse.py; see
+// tvb_coarse_nd in include/topovox_b200.h). Coarse vectors are in ND order.
 struct CoarseNDDev {
-  int n_nodes, height, max_front;
-  const long long* meta;      // [n_nodes][8]: s, u, g_off, z_off, sdof_off, udof_off, child_begin, child_end
+  int n_levels;               // bottom tree heights 0..n_levels-1 (node-wise LDL^T)
+  int max_front, max_sep;
+  const long long* meta;      // [bottom node][8]: s, u, g_off, z_off, sd_off (ND dof), ud_off, child_begin, child_end
   const long long* children;  // [n_child][2]: child node, cmap offset
   const int* cmap;            // child U position -> parent front position
   const double* G;            // per node u x s, row-major (G = F_US F_SS^-1)
   const double* Gt;           // per node s x u, row-major (G^T)
   const double* Z;            // per node s x s, row-major (F_SS^-1)
-  const int* sdof;            // per node: separator coarse DOFs
-  const int* udof;            // per node: update-set coarse DOFs
-  double* fS;                 // per node scratch: assembled separator rhs
+  const int* udof;            // per node: update-set coarse DOFs (ND numbering)
+  double* fS;                 // ND-dof indexed scratch: assembled separator rhs
   double* cU;                 // per node scratch: update vector passed to the parent
   const int* fwd_items;       // [n][3] (node, row0, row1), grouped by height (leaves first)
-  const int* bwd_items;       // [n][3], grouped by height (root first)
-  const long long* fwd_ptr;   // host: height+2 group offsets
+  const int* bwd_items;       // [n][3], grouped by height (top bottom level first)
+  const long long* fwd_ptr;   // host: n_levels+1 group offsets
   const long long* bwd_ptr;   // host
   const int* split;           // host, per height: 1 = separate assembly pass (large fronts)
   const int* asm_nodes;       // device: nodes grouped by height (assembly pass)
-  const long long* asm_ptr;   // host: height+2 offsets into asm_nodes
-  int max_sep;                // largest separator (smem of the row pass)
+  const long long* asm_ptr;   // host
+  // dense top (heights >= n_levels): x_T = S_T^-1 (y_T + children)
+  int n_top;
+  long long top_off;          // ND dof offset of the top set
+  const double* ZT;           // n_top x n_top
+  double* fT;                 // scratch n_top
+  int n_tchildren;
+  const long long* tchildren; // [n][2]: bottom node, tmap offset
+  const int* tmap;            // child U position -> top position
+  const int* perm;            // natural block -> ND block (restriction / prolongation)
 };
 
 cudaError_t launch_coarse_nd(const CoarseNDDev& D, const double* y, double* x, const int* stop, cudaStream_t s);

@@ -217,9 +217,10 @@ __global__ void __launch_bounds__(kRestrictThreads) k_restrict(Agglo A, const ui
   if (stop != nullptr && *stop) return;
   const double beta = (y2 != nullptr) ? st->beta : 0.0;  // restrict y + beta*y2
   const long long B = blockIdx.x;
+  const long long PB = D.perm != nullptr ? (long long)D.perm[B] : B;  // coarse-vector position
   const int keep = D.keep[B];
   if (keep == 0) {
-    if (threadIdx.x < 6) yc[6 * B + threadIdx.x] = 0.0;
+    if (threadIdx.x < 6) yc[6 * PB + threadIdx.x] = 0.0;
     return;
   }
   int bx, by, bz, nxl, nyl, nzl;
@@ -262,7 +263,7 @@ __global__ void __launch_bounds__(kRestrictThreads) k_restrict(Agglo A, const ui
     const double* S = D.S + 36 * B;
     double v = 0.0;
     for (int i = 0; i < 6; ++i) v = fma(S[i + 6 * j], m[i], v);
-    yc[6 * B + j] = v;
+    yc[6 * PB + j] = v;
   }
 }
 
@@ -273,20 +274,22 @@ cudaError_t launch_restrict(const Agglo& A, const uint8_t* nflags, DeflData D, c
 }
 
 // nu_B = S_B mu_B
-__global__ void k_block_nu(long long nb, const double* S, const double* mu, double* nu, const int* stop) {
+__global__ void k_block_nu(long long nb, const double* S, const int* perm, const double* mu, double* nu,
+                           const int* stop) {
   if (stop != nullptr && *stop) return;
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= 6 * nb) return;
   const long long B = t / 6;
+  const long long PB = perm != nullptr ? (long long)perm[B] : B;
   const int i = (int)(t % 6);
   double v = 0.0;
-  for (int j = 0; j < 6; ++j) v = fma(S[36 * B + i + 6 * j], mu[6 * B + j], v);
+  for (int j = 0; j < 6; ++j) v = fma(S[36 * B + i + 6 * j], mu[6 * PB + j], v);
   nu[t] = v;
 }
 
 cudaError_t launch_block_nu(const Agglo& A, DeflData D, const double* mu, double* nu, cudaStream_t s,
                             const int* stop) {
-  k_block_nu<<<(unsigned)((6 * A.nb + 255) / 256), 256, 0, s>>>(A.nb, D.S, mu, nu, stop);
+  k_block_nu<<<(unsigned)((6 * A.nb + 255) / 256), 256, 0, s>>>(A.nb, D.S, D.perm, mu, nu, stop);
   return cudaGetLastError();
 }
 

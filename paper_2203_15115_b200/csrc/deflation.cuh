@@ -38,10 +38,13 @@ inline Agglo make_agglo(const Grid& g, int b, double h) {
 //                   topovox/fea.py:141-155; S orthonormalises them like the
 //                   per-block QR of topovox/fea.py:156-160, zero for dropped)
 //   keep[B]        bit j set <=> column j kept (|R_jj| > 1e-10 max |R_ii|)
+//   perm[B]        coarse-vector block position of block B (the ND order of
+//                  the sparse coarse factor); nullptr = natural order
 struct DeflData {
   double* cen;
   double* S;
   int* keep;
+  const int* perm = nullptr;
 };
 
 cudaError_t launch_node_flags(const Grid& G, const long long* fixed_dofs, long long nfixed, const double* occ,

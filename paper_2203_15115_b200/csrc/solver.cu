@@ -122,6 +122,7 @@ int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
   }
   PcgWork W = carve(P.ws, G, defl ? P.block : 0);
   DeflData D{const_cast<double*>(P.cen), const_cast<double*>(P.S), const_cast<int*>(P.keep)};
+  if (P.coarse_kind == 1) D.perm = P.nd.perm;  // coarse vectors in the factor's ND order
 
   int dev = 0;
   TVB_CK(cudaGetDevice(&dev));

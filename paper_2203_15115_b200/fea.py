@@ -273,7 +273,10 @@ class DeflationSpace:
         full = torch.zeros(6 * self.n_blocks, dtype=torch.float64, device="cuda")
         full[mask] = r
         if self.nd is not None:
-            sol = self.nd.solve_device(full, torch.empty_like(full))
+            ndi = torch.from_numpy(self.nd.nd_index()).cuda()
+            y = torch.empty_like(full)
+            y[ndi] = full                                   # natural -> ND order
+            sol = self.nd.solve_device(y, torch.empty_like(full))[ndi]
         else:
             sol = self.coarse_inv @ full
         return to_host_if(sol[mask], np_in)

@@ -52,7 +52,7 @@ for name in which:
     out[name] = {"n_dofs": d.n_dofs, "n_coarse": defl.n_vectors, "basis_s": round(t_basis, 3), "prepare_s": round(t_prep, 3),
                  "iters": r.iterations, "solve_ms": round(ms, 2), "us_per_iter": round(1e3 * ms / max(1, r.iterations), 1),
                  "factor_GB": round(defl.nd.bytes / 1e9, 3) if defl.nd is not None else None,
-                 "nd_height": defl.nd.height if defl.nd is not None else None,
+                 "nd_levels": defl.nd.H0 if defl.nd is not None else None, "n_top": defl.nd.n_top if defl.nd is not None else None,
                  "J": float(fd @ r.u), "max_mem_GB": round(torch.cuda.max_memory_allocated() / 1e9, 2),
                  "total_s": round(time.perf_counter() - t_all, 2)}
     print(json.dumps({name: out[name]}), flush=True)

@@ -22,4 +22,4 @@ x = torch.empty_like(y)
 for _ in range(3):
     defl.nd.solve_device(y, x)
 torch.cuda.synchronize()
-print("ok", defl.nd.height)
+print("ok", defl.nd.H0, defl.nd.n_top)

@@ -46,40 +46,50 @@ def dense_of(Es, mx, my, mz):
 
 
 def emulate_solve(nd, y):
-    """numpy twin of k_coarse_fwd / k_coarse_bwd over the packed device data."""
+    """numpy twin of the device solve (coarse.cu) over the packed data; y and
+    the result are in ND order."""
     meta = nd.meta.numpy()
     ch = nd.children.numpy()
     cmap = nd.cmap.numpy()
-    G, Gt, Z = nd.G.numpy(), nd.Gt.numpy(), nd.Z.numpy()
-    sdof, udof = nd.s_dof.numpy(), nd.u_dof.numpy()
+    G, Gt, Z, ZT = nd.G.numpy(), nd.Gt.numpy(), nd.Z.numpy(), nd.ZT.numpy()
+    udof = nd.udof.numpy()
     fS = np.zeros(nd.fS.numel())
     cU = np.zeros(nd.cU.numel())
     fwd, bwd = nd.fwd_items.numpy(), nd.bwd_items.numpy()
-    done = set()
-    for node, r0, r1 in fwd:
-        s, u, g, z, so, uo, cb, ce = meta[node]
-        f = np.concatenate([y[sdof[so:so + s]], np.zeros(u)])
-        for k in range(cb, ce):
-            cn, co = ch[k]
-            cu = meta[cn][1]
-            f[cmap[co:co + cu]] += cU[meta[cn][5]:meta[cn][5] + cu]
-        if node not in done:
+    for h in range(nd.H0):  # k_coarse_fwd (or k_coarse_asm + k_coarse_rows)
+        for node, r0, r1 in fwd[nd.fwd_ptr[h]:nd.fwd_ptr[h + 1]]:
+            s, u, g, z, so, uo, cb, ce = meta[node]
+            f = np.concatenate([y[so:so + s], np.zeros(u)])
+            for k in range(cb, ce):
+                cn, co = ch[k]
+                cu = meta[cn][1]
+                f[cmap[co:co + cu]] += cU[meta[cn][5]:meta[cn][5] + cu]
             fS[so:so + s] = f[:s]
-            done.add(node)
-        Gm = G[g:g + s * u].reshape(u, s)
-        cU[uo + r0:uo + r1] = f[s + r0:s + r1] - Gm[r0:r1] @ f[:s]
+            Gm = G[g:g + s * u].reshape(u, s)
+            cU[uo + r0:uo + r1] = f[s + r0:s + r1] - Gm[r0:r1] @ f[:s]
     x = np.zeros_like(y)
-    for node, r0, r1 in bwd:
+    if nd.n_top:  # k_coarse_top_asm + k_coarse_top_rows
+        n = nd.n_top
+        fT = y[nd.top_off:].copy()
+        tch, tmap = nd.tchildren.numpy(), nd.tmap.numpy()
+        for k in range(nd.n_tchildren):
+            cn, to = tch[k]
+            cu = meta[cn][1]
+            fT[tmap[to:to + cu]] += cU[meta[cn][5]:meta[cn][5] + cu]
+        x[nd.top_off:] = ZT[:n * n].reshape(n, n) @ fT
+    for node, r0, r1 in bwd:  # k_coarse_bwd, top-most bottom level first
         s, u, g, z, so, uo, cb, ce = meta[node]
         Zm = Z[z:z + s * s].reshape(s, s)
         Gtm = Gt[g:g + s * u].reshape(s, u)
         xu = x[udof[uo:uo + u]]
-        x[sdof[so + r0:so + r1]] = Zm[r0:r1] @ fS[so:so + s] - (Gtm[r0:r1] @ xu if u else 0.0)
+        x[so + r0:so + r1] = Zm[r0:r1] @ fS[so:so + s] - (Gtm[r0:r1] @ xu if u else 0.0)
     return x
 
 
-@pytest.mark.parametrize("grid,leaf", [((5, 5, 10), 27), ((4, 3, 2), 2), ((7, 1, 3), 4), ((1, 1, 1), 27)])
-def test_nd_factor_matches_dense(grid, leaf):
+@pytest.mark.parametrize("top_max", [0, 60, 4608])
+@pytest.mark.parametrize("grid,leaf", [((5, 5, 10), 27), ((4, 3, 2), 2), ((7, 1, 3), 4), ((1, 1, 1), 27),
+                                       ((9, 8, 7), 8)])
+def test_nd_factor_matches_dense(grid, leaf, top_max):
     from paper_2203_15115_b200.coarse import NDCoarseSolver, nested_dissection
 
     mx, my, mz = grid
@@ -90,8 +100,15 @@ def test_nd_factor_matches_dense(grid, leaf):
     # every block is in exactly one separator
     allsep = np.concatenate([n.sep for n in nodes])
     assert np.array_equal(np.sort(allsep), np.arange(mx * my * mz))
-    nd = NDCoarseSolver(grid, torch.from_numpy(Es.reshape(-1)), leaf_max=leaf, make_desc=False)
+    nd = NDCoarseSolver(grid, torch.from_numpy(Es.reshape(-1)), leaf_max=leaf, top_max=top_max,
+                        make_desc=False)
+    assert nd.n_top <= max(top_max, 0) or nd.H0 == max(n.height for n in nodes) + 1
+    # the ND order is a permutation; separators are contiguous
+    assert np.array_equal(np.sort(nd.perm_host), np.arange(mx * my * mz))
     y = np.random.default_rng(1).standard_normal(E.shape[0])
-    x = emulate_solve(nd, y)
+    ndi = nd.nd_index()
+    yn = np.empty_like(y)
+    yn[ndi] = y
+    x = emulate_solve(nd, yn)[ndi]
     ref = np.linalg.solve(E, y)
     assert np.abs(x - ref).max() <= 1e-12 * np.abs(ref).max()
