@@ -127,31 +127,31 @@ int tvb_coarse_dense(int nx, int ny, int nz, int block, const double* d_Es, doub
 typedef struct tvb_coarse_nd {
   int n_levels;             /* bottom tree heights factored node by node */
   int max_front, max_sep;
-  const long long* d_meta;  /* [bottom node][8] s,u,g_off,z_off,sd_off,ud_off,child_begin,child_end */
-  const long long* d_children;
-  const int* d_cmap;
-  const double* d_G;
-  const double* d_Gt;
-  const double* d_Z;
+  const long long* d_meta;  /* [bottom node][8] s,u,g_off,b_off,sd_off,ud_off,gm_off,0 */
+  const int* d_gmap;        /* per node (s+u) x 2: children's update-vector index per front position, -1 = none */
+  const double* d_G;        /* per node u x s (G = F_US F_SS^-1) */
+  const double* d_B;        /* per node s x (s+u): [F_SS^-1 | -G^T] */
   const int* d_udof;
   double* d_fS;
   double* d_cU;
-  const int* d_fwd_items;
+  const int* d_fwd_items;   /* (node, row0, row1) */
   const int* d_bwd_items;
   const long long* h_fwd_ptr;  /* n_levels+1 work-item group offsets */
   const long long* h_bwd_ptr;
+  const int* h_fwd_wpr;     /* warps per row per group (1,2,4,8) */
+  const int* h_bwd_wpr;
   const int* h_split;       /* per height: 1 = separate front-assembly launch (large fronts) */
   const int* d_asm_nodes;   /* nodes grouped by height */
   const long long* h_asm_ptr;
   int n_top;                /* dense top set (heights >= n_levels), DOFs */
   long long top_off;        /* its ND DOF offset (= 6 Nb - n_top) */
+  int top_wpr;
   const double* d_ZT;       /* n_top x n_top inverse of the top Schur complement */
   double* d_fT;
-  int n_tchildren;
-  const long long* d_tchildren;
-  const int* d_tmap;
+  const int* d_tptr;        /* CSR over top positions of children's update-vector entries */
+  const int* d_tidx;
   const int* d_perm;        /* i32[Nb]: natural block -> ND block */
-  const double* d_factor;   /* the single allocation holding G, G^T, Z, ZT (L2 persistence window) */
+  const double* d_factor;   /* the single allocation holding G, B, ZT (L2 persistence window) */
   size_t factor_bytes;
 } tvb_coarse_nd;
 int tvb_coarse_nd_solve(const tvb_coarse_nd* nd, const double* d_y, double* d_x, void* stream);

@@ -25,15 +25,13 @@ c_int, c_double, c_size_t, c_ll, P = ctypes.c_int, ctypes.c_double, ctypes.c_siz
 class CoarseND(ctypes.Structure):
     _fields_ = [
         ("n_levels", c_int), ("max_front", c_int), ("max_sep", c_int),
-        ("d_meta", P), ("d_children", P), ("d_cmap", P),
-        ("d_G", P), ("d_Gt", P), ("d_Z", P),
+        ("d_meta", P), ("d_gmap", P), ("d_G", P), ("d_B", P),
         ("d_udof", P), ("d_fS", P), ("d_cU", P),
         ("d_fwd_items", P), ("d_bwd_items", P),
-        ("h_fwd_ptr", P), ("h_bwd_ptr", P),
+        ("h_fwd_ptr", P), ("h_bwd_ptr", P), ("h_fwd_wpr", P), ("h_bwd_wpr", P),
         ("h_split", P), ("d_asm_nodes", P), ("h_asm_ptr", P),
-        ("n_top", c_int), ("top_off", ctypes.c_longlong),
-        ("d_ZT", P), ("d_fT", P),
-        ("n_tchildren", c_int), ("d_tchildren", P), ("d_tmap", P),
+        ("n_top", c_int), ("top_off", ctypes.c_longlong), ("top_wpr", c_int),
+        ("d_ZT", P), ("d_fT", P), ("d_tptr", P), ("d_tidx", P),
         ("d_perm", P),
         ("d_factor", P), ("factor_bytes", c_size_t),
     ]

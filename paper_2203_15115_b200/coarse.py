@@ -22,7 +22,10 @@ so it is factored here by geometric nested dissection:
 * solve (device, every CG iteration, hand-written kernels in coarse.cu):
       forward, bottom heights 0..H0-1:  f_S = y_S + sum(children c|S), c_U = f_U - G f_S
       top:                              x_T = S_T^-1 (y_T + sum(children c|T))
-      backward, heights H0-1..0:        x_S = Z f_S - G^T x_U
+      backward, heights H0-1..0:        x_S = [Z | -G^T] [f_S ; x_U]   (one stored s x (s+u) row block)
+  Front vectors are gathered (each front position lists its children's
+  update-vector entries), so assembly needs no barriers or atomics, and long
+  matrix rows are split across several warps (the solve is latency-bound).
   The exact coarse solve keeps the DPCG iterates identical (up to rounding) to
   the reference's dense Cholesky.
 
@@ -48,6 +51,10 @@ SPLIT_FRONT = int(os.environ.get("TVB_ND_SPLIT_FRONT", "2048"))
 #: largest top set inverted densely (DOFs); the top tree levels it replaces
 #: would otherwise cost two latency-bound launches each
 TOP_MAX = int(os.environ.get("TVB_ND_TOP_MAX", "4608"))
+#: target warps per solve launch (148 SMs x 16)
+WARPS_IN_FLIGHT = int(os.environ.get("TVB_ND_WARPS", "2368"))
+#: dynamic shared memory per CTA (B200: 227 KB opt-in)
+SMEM_MAX = 227 * 1024
 
 
 @dataclass
@@ -189,9 +196,10 @@ class NDCoarseSolver:
         nb = self.nb
         E6 = Es.view(nb, 27, 6, 6)
         upd = {}
-        G_list, Z_list = [], []
-        s_list, u_list, sd_list, udof_list, cmaps, children = [], [], [], [], [], []
-        child_ptr = [0]
+        ud_off = {}
+        ud_cursor = 0
+        G_list, B_list = [], []
+        s_list, u_list, sd_list, udof_list, gmaps = [], [], [], [], []
         blk_cursor = 0
         for ni in bottom:
             n = nodes[ni]
@@ -202,14 +210,16 @@ class NDCoarseSolver:
             F = torch.zeros((6 * front.size, 6 * front.size), dtype=torch.float64, device=dev)
             rows, cols, srcB, srcD = self._stencil_entries(n.sep, pos)
             self._scatter_blocks(torch, F, E6, rows, cols, srcB, srcD, mirror_from=ns)
-            for c in n.children:
+            # gather map: front position -> (child 0, child 1) update-vector index
+            gm = -np.ones((6 * front.size, 2), dtype=np.int64)
+            assert len(n.children) <= 2
+            for k, c in enumerate(n.children):
                 m = _dofs(pos[nodes[c].upd])
                 Uc = upd.pop(c)
                 mt = torch.from_numpy(m).to(dev)
                 F[mt[:, None], mt[None, :]] += Uc
-                cmaps.append(m.astype(np.int32))
-                children.append(bidx[c])
-            child_ptr.append(len(children))
+                gm[m, k] = ud_off[c] + np.arange(m.size)
+            gmaps.append(gm.astype(np.int32).ravel())
             S = 6 * ns
             L, info = torch.linalg.cholesky_ex(0.5 * (F[:S, :S] + F[:S, :S].T))
             if int(info.item()) != 0:
@@ -218,17 +228,19 @@ class NDCoarseSolver:
             G = F[S:, :S] @ Z
             if nu:
                 upd[ni] = F[S:, S:] - G @ F[:S, S:]
-            Z_list.append(Z.contiguous())
             G_list.append(G.contiguous())
+            B_list.append(torch.cat([Z, -G.T], dim=1).contiguous())   # x_S = [Z | -G^T] [f_S ; x_U]
             s_list.append(S)
             u_list.append(6 * nu)
             sd_list.append(6 * blk_cursor)
+            ud_off[ni] = ud_cursor
+            ud_cursor += 6 * nu
             blk_cursor += ns
             udof_list.append(_dofs(perm[n.upd]).astype(np.int32))
             del F
         # ---- dense top: S_T = E_TT + updates of bottom nodes with a top parent
         self.Ztop = None
-        tchildren, tmaps = [], []
+        t_pos, t_idx = [], []
         if self.n_top:
             tblocks = np.concatenate([nodes[i].sep for i in top]).astype(np.int64)
             tpos = -np.ones(nb, dtype=np.int64)
@@ -242,93 +254,118 @@ class NDCoarseSolver:
                     m = _dofs(tpos[nodes[ni].upd])
                     mt = torch.from_numpy(m).to(dev)
                     ST[mt[:, None], mt[None, :]] += upd.pop(ni)
-                    tchildren.append(bidx[ni])
-                    tmaps.append(m.astype(np.int32))
+                    t_pos.append(m)
+                    t_idx.append(ud_off[ni] + np.arange(m.size))
             L, info = torch.linalg.cholesky_ex(0.5 * (ST + ST.T))
             if int(info.item()) != 0:
                 raise np.linalg.LinAlgError("coarse top Schur complement not SPD")
             self.Ztop = torch.cholesky_inverse(L).contiguous()
             del ST, L
         assert not upd, "unconsumed update matrices"
-        self._pack(torch, dev, G_list, Z_list, np.array(s_list, np.int64), np.array(u_list, np.int64),
-                   np.array(sd_list, np.int64), udof_list, cmaps, child_ptr, children, tchildren, tmaps,
+        self._pack(torch, dev, G_list, B_list, np.array(s_list, np.int64), np.array(u_list, np.int64),
+                   np.array(sd_list, np.int64), udof_list, gmaps, t_pos, t_idx, ud_cursor,
                    [nodes[i].height for i in bottom])
 
-    def _pack(self, torch, dev, G_list, Z_list, s, u, sd, udof_list, cmaps, child_ptr, children, tchildren,
-              tmaps, heights):
+    @staticmethod
+    def _wpr(rowlen: int, rows: int) -> int:
+        """warps per matrix row (1, 2, 4, 8) for a launch of ``rows`` rows of
+        length ``rowlen``: rows are split across warps only until the launch
+        has enough warps in flight (small levels are latency-bound); every
+        split costs one more shared-memory copy of the right-hand vector per
+        row, which dominates once the level is bandwidth-bound."""
+        forced = os.environ.get("TVB_ND_WPR")
+        if forced:
+            return int(forced)
+        w = 1
+        while w < 8 and rows * w < WARPS_IN_FLIGHT and rowlen >= 256 * w:
+            w *= 2
+        return w
+
+    def _pack(self, torch, dev, G_list, B_list, s, u, sd, udof_list, gmaps, t_pos, t_idx, n_cu, heights):
         nbot = len(G_list)
         self.n_bottom = nbot
         self.s, self.u = s, u
         g_off = np.zeros(nbot + 1, dtype=np.int64)
-        z_off = np.zeros(nbot + 1, dtype=np.int64)
+        b_off = np.zeros(nbot + 1, dtype=np.int64)
         if nbot:
             g_off[1:] = np.cumsum(s * u)
-            z_off[1:] = np.cumsum(s * s)
-        ng, nz = int(g_off[-1]), int(z_off[-1])
+            b_off[1:] = np.cumsum(s * (s + u))
+        ng, nbb = int(g_off[-1]), int(b_off[-1])
         ntop2 = self.n_top * self.n_top
-        # G, G^T, Z and the dense top inverse in ONE allocation
-        self.factor = torch.zeros(2 * ng + nz + ntop2 + 4, dtype=torch.float64, device=dev)
+        # G, [Z | -G^T] and the dense top inverse in ONE allocation
+        self.factor = torch.zeros(ng + nbb + ntop2 + 3, dtype=torch.float64, device=dev)
         self.G = self.factor[:ng + 1]
-        self.Gt = self.factor[ng + 1:2 * ng + 2]
-        self.Z = self.factor[2 * ng + 2:2 * ng + nz + 3]
-        self.ZT = self.factor[2 * ng + nz + 3:]
+        self.B = self.factor[ng + 1:ng + nbb + 2]
+        self.ZT = self.factor[ng + nbb + 2:]
         if ng:
             self.G[:ng] = torch.cat([g.reshape(-1) for g in G_list])
-            self.Gt[:ng] = torch.cat([g.T.contiguous().reshape(-1) for g in G_list])
-        if nz:
-            self.Z[:nz] = torch.cat([z.reshape(-1) for z in Z_list])
+        if nbb:
+            self.B[:nbb] = torch.cat([b.reshape(-1) for b in B_list])
         if ntop2:
             self.ZT[:ntop2] = self.Ztop.reshape(-1)
         self.Ztop = None
         ud_off = np.zeros(nbot + 1, dtype=np.int64)
         if nbot:
             ud_off[1:] = np.cumsum(u)
+        assert int(ud_off[-1]) == n_cu
         self.udof = torch.from_numpy(np.concatenate(udof_list + [np.zeros(1, np.int32)])).to(dev)
-        cm_off = np.zeros(len(cmaps) + 1, dtype=np.int64)
-        cm_off[1:] = np.cumsum([c.size for c in cmaps])
-        self.cmap = torch.from_numpy(np.concatenate(cmaps + [np.zeros(1, np.int32)])).to(dev)
+        gm_off = np.zeros(nbot + 1, dtype=np.int64)
+        gm_off[1:] = np.cumsum([g.size for g in gmaps])
+        self.gmap = torch.from_numpy(np.concatenate(gmaps + [np.zeros(1, np.int32)])).to(dev)
         meta = np.zeros((max(nbot, 1), 8), dtype=np.int64)
         if nbot:
-            meta[:] = np.stack([s, u, g_off[:-1], z_off[:-1], sd, ud_off[:-1], np.array(child_ptr[:-1]),
-                                np.array(child_ptr[1:])], axis=1)
+            meta[:, :7] = np.stack([s, u, g_off[:-1], b_off[:-1], sd, ud_off[:-1], gm_off[:-1]], axis=1)
         self.meta = torch.from_numpy(np.ascontiguousarray(meta)).to(dev)
-        ch = np.stack([np.array(children, dtype=np.int64), cm_off[:-1]], axis=1) if children else \
-            np.zeros((1, 2), dtype=np.int64)
-        self.children = torch.from_numpy(np.ascontiguousarray(ch)).to(dev)
-        tm_off = np.zeros(len(tmaps) + 1, dtype=np.int64)
-        tm_off[1:] = np.cumsum([t.size for t in tmaps])
-        self.tmap = torch.from_numpy(np.concatenate(tmaps + [np.zeros(1, np.int32)])).to(dev)
-        tch = np.stack([np.array(tchildren, dtype=np.int64), tm_off[:-1]], axis=1) if tchildren else \
-            np.zeros((1, 2), dtype=np.int64)
-        self.tchildren = torch.from_numpy(np.ascontiguousarray(tch)).to(dev)
-        self.n_tchildren = len(tchildren)
+        # top gather (CSR over top positions, contributions in child order)
+        if t_pos:
+            tp, ti = np.concatenate(t_pos), np.concatenate(t_idx)
+            o = np.argsort(tp, kind="stable")
+            tp, ti = tp[o], ti[o]
+        else:
+            tp, ti = np.zeros(0, np.int64), np.zeros(0, np.int64)
+        tptr = np.zeros(self.n_top + 1, dtype=np.int64)
+        np.add.at(tptr, tp + 1, 1)
+        tptr = np.cumsum(tptr)
+        self.tptr = torch.from_numpy(tptr.astype(np.int32)).to(dev)
+        self.tidx = torch.from_numpy(np.concatenate([ti, [0]]).astype(np.int32)).to(dev)
         n_c = 6 * self.nb
         self.fS = torch.zeros(n_c + 1, dtype=torch.float64, device=dev)   # indexed by ND dof
-        self.cU = torch.zeros(int(ud_off[-1]) + 1, dtype=torch.float64, device=dev)
+        self.cU = torch.zeros(n_cu + 1, dtype=torch.float64, device=dev)
         self.fT = torch.zeros(self.n_top + 1, dtype=torch.float64, device=dev)
         self.perm = torch.from_numpy(self.perm_host.astype(np.int32)).to(dev)
-        # work items per bottom height: (node, row0, row1); fwd rows = u, bwd rows = s; 8 rows = 1 per warp
+        # work items per bottom height: (node, row0, row1); fwd rows = u (length s),
+        # bwd rows = s (length s + u); 8 / wpr rows per 256-thread CTA
         heights = np.array(heights, dtype=np.int64)
-        step = 8
-        fwd, bwd, fptr, bptr = [], [], [0], [0]
+        fwd, bwd, fptr, bptr, fw, bw = [], [], [0], [0], [], []
         for h in range(self.H0):
-            for ni in np.flatnonzero(heights == h):
+            at = np.flatnonzero(heights == h)
+            w = self._wpr(int(s[at].max()) if at.size else 1, int(u[at].sum()))
+            fw.append(w)
+            for ni in at:
                 nr = int(u[ni])
-                for r0 in range(0, max(nr, 1), step):
-                    fwd.append((ni, r0, min(nr, r0 + step)))
+                for r0 in range(0, max(nr, 1), 8 // w):
+                    fwd.append((ni, r0, min(nr, r0 + 8 // w)))
             fptr.append(len(fwd))
         for h in range(self.H0 - 1, -1, -1):
-            for ni in np.flatnonzero(heights == h):
+            at = np.flatnonzero(heights == h)
+            w = self._wpr(int((s[at] + u[at]).max()) if at.size else 1, int(s[at].sum()))
+            bw.append(w)
+            for ni in at:
                 nr = int(s[ni])
-                for r0 in range(0, nr, step):
-                    bwd.append((ni, r0, min(nr, r0 + step)))
+                for r0 in range(0, nr, 8 // w):
+                    bwd.append((ni, r0, min(nr, r0 + 8 // w)))
             bptr.append(len(bwd))
+        self.top_wpr = self._wpr(self.n_top, self.n_top)
         self.fwd_items = torch.from_numpy(np.array(fwd or [(0, 0, 0)], dtype=np.int32).reshape(-1, 3)).to(dev)
         self.bwd_items = torch.from_numpy(np.array(bwd or [(0, 0, 0)], dtype=np.int32).reshape(-1, 3)).to(dev)
         self.fwd_ptr = np.array(fptr, dtype=np.int64)
         self.bwd_ptr = np.array(bptr, dtype=np.int64)
+        self.fwd_wpr = np.array(fw or [1], dtype=np.int32)
+        self.bwd_wpr = np.array(bw or [1], dtype=np.int32)
         self.max_front = int((s + u).max()) if nbot else 1
         self.max_sep = int(s.max()) if nbot else 1
+        if 8 * max(self.max_front, self.n_top + 1) > SMEM_MAX:
+            raise ValueError(f"coarse front of {max(self.max_front, self.n_top)} DOFs exceeds shared memory")
         self.split = np.array([int(max(int(s[i] + u[i]) for i in np.flatnonzero(heights == h)) > SPLIT_FRONT)
                                for h in range(self.H0)] or [0], dtype=np.int32)
         asm, aptr = [], [0]
@@ -339,28 +376,32 @@ class NDCoarseSolver:
         self.asm_ptr = np.array(aptr, dtype=np.int64)
         self.bytes = self.factor.numel() * 8
 
+    def _host_array(self, ctype, values):
+        arr = (ctype * len(values))(*values)
+        self._keep.append(arr)
+        return ctypes.cast(arr, ctypes.c_void_p)
+
     def _make_desc(self):
         from ._lib import CoarseND
 
+        self._keep = []
         d = CoarseND()
         d.n_levels = self.H0
         d.max_front, d.max_sep = self.max_front, self.max_sep
-        d.d_meta, d.d_children, d.d_cmap = ptr(self.meta), ptr(self.children), ptr(self.cmap)
-        d.d_G, d.d_Gt, d.d_Z = ptr(self.G), ptr(self.Gt), ptr(self.Z)
+        d.d_meta, d.d_gmap = ptr(self.meta), ptr(self.gmap)
+        d.d_G, d.d_B = ptr(self.G), ptr(self.B)
         d.d_udof, d.d_fS, d.d_cU = ptr(self.udof), ptr(self.fS), ptr(self.cU)
         d.d_fwd_items, d.d_bwd_items = ptr(self.fwd_items), ptr(self.bwd_items)
-        self._fptr = (ctypes.c_longlong * len(self.fwd_ptr))(*self.fwd_ptr.tolist())
-        self._bptr = (ctypes.c_longlong * len(self.bwd_ptr))(*self.bwd_ptr.tolist())
-        d.h_fwd_ptr = ctypes.cast(self._fptr, ctypes.c_void_p)
-        d.h_bwd_ptr = ctypes.cast(self._bptr, ctypes.c_void_p)
-        self._split = (ctypes.c_int * len(self.split))(*self.split.tolist())
-        self._aptr = (ctypes.c_longlong * len(self.asm_ptr))(*self.asm_ptr.tolist())
-        d.h_split = ctypes.cast(self._split, ctypes.c_void_p)
+        d.h_fwd_ptr = self._host_array(ctypes.c_longlong, self.fwd_ptr.tolist())
+        d.h_bwd_ptr = self._host_array(ctypes.c_longlong, self.bwd_ptr.tolist())
+        d.h_fwd_wpr = self._host_array(ctypes.c_int, self.fwd_wpr.tolist())
+        d.h_bwd_wpr = self._host_array(ctypes.c_int, self.bwd_wpr.tolist())
+        d.h_split = self._host_array(ctypes.c_int, self.split.tolist())
         d.d_asm_nodes = ptr(self.asm_nodes)
-        d.h_asm_ptr = ctypes.cast(self._aptr, ctypes.c_void_p)
-        d.n_top, d.top_off = self.n_top, self.top_off
+        d.h_asm_ptr = self._host_array(ctypes.c_longlong, self.asm_ptr.tolist())
+        d.n_top, d.top_off, d.top_wpr = self.n_top, self.top_off, self.top_wpr
         d.d_ZT, d.d_fT = ptr(self.ZT), ptr(self.fT)
-        d.n_tchildren, d.d_tchildren, d.d_tmap = self.n_tchildren, ptr(self.tchildren), ptr(self.tmap)
+        d.d_tptr, d.d_tidx = ptr(self.tptr), ptr(self.tidx)
         d.d_perm = ptr(self.perm)
         d.d_factor, d.factor_bytes = ptr(self.factor), self.bytes
         return d

@@ -110,11 +110,9 @@ static CoarseNDDev coarse_nd_dev(const tvb_coarse_nd* d) {
   D.max_front = d->max_front;
   D.max_sep = d->max_sep;
   D.meta = d->d_meta;
-  D.children = d->d_children;
-  D.cmap = d->d_cmap;
+  D.gmap = d->d_gmap;
   D.G = d->d_G;
-  D.Gt = d->d_Gt;
-  D.Z = d->d_Z;
+  D.B = d->d_B;
   D.udof = d->d_udof;
   D.fS = d->d_fS;
   D.cU = d->d_cU;
@@ -122,16 +120,18 @@ static CoarseNDDev coarse_nd_dev(const tvb_coarse_nd* d) {
   D.bwd_items = d->d_bwd_items;
   D.fwd_ptr = d->h_fwd_ptr;
   D.bwd_ptr = d->h_bwd_ptr;
+  D.fwd_wpr = d->h_fwd_wpr;
+  D.bwd_wpr = d->h_bwd_wpr;
   D.split = d->h_split;
   D.asm_nodes = d->d_asm_nodes;
   D.asm_ptr = d->h_asm_ptr;
   D.n_top = d->n_top;
   D.top_off = d->top_off;
+  D.top_wpr = d->top_wpr;
   D.ZT = d->d_ZT;
   D.fT = d->d_fT;
-  D.n_tchildren = d->n_tchildren;
-  D.tchildren = d->d_tchildren;
-  D.tmap = d->d_tmap;
+  D.tptr = d->d_tptr;
+  D.tidx = d->d_tidx;
   D.perm = d->d_perm;
   return D;
 }

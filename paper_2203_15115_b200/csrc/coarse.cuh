@@ -8,12 +8,10 @@ namespace tvb {
 struct CoarseNDDev {
   int n_levels;               // bottom tree heights 0..n_levels-1 (node-wise LDL^T)
   int max_front, max_sep;
-  const long long* meta;      // [bottom node][8]: s, u, g_off, z_off, sd_off (ND dof), ud_off, child_begin, child_end
-  const long long* children;  // [n_child][2]: child node, cmap offset
-  const int* cmap;            // child U position -> parent front position
+  const long long* meta;      // [bottom node][8]: s, u, g_off, b_off, sd_off (ND dof), ud_off, gm_off, 0
+  const int* gmap;            // per node [(s+u)][2]: children's cU index per front position (-1 = none)
   const double* G;            // per node u x s, row-major (G = F_US F_SS^-1)
-  const double* Gt;           // per node s x u, row-major (G^T)
-  const double* Z;            // per node s x s, row-major (F_SS^-1)
+  const double* B;            // per node s x (s+u), row-major: [F_SS^-1 | -G^T]
   const int* udof;            // per node: update-set coarse DOFs (ND numbering)
   double* fS;                 // ND-dof indexed scratch: assembled separator rhs
   double* cU;                 // per node scratch: update vector passed to the parent
@@ -21,17 +19,19 @@ struct CoarseNDDev {
   const int* bwd_items;       // [n][3], grouped by height (top bottom level first)
   const long long* fwd_ptr;   // host: n_levels+1 group offsets
   const long long* bwd_ptr;   // host
+  const int* fwd_wpr;         // host, per group: warps per matrix row (1, 2, 4, 8)
+  const int* bwd_wpr;         // host
   const int* split;           // host, per height: 1 = separate assembly pass (large fronts)
   const int* asm_nodes;       // device: nodes grouped by height (assembly pass)
   const long long* asm_ptr;   // host
   // dense top (heights >= n_levels): x_T = S_T^-1 (y_T + children)
   int n_top;
   long long top_off;          // ND dof offset of the top set
+  int top_wpr;
   const double* ZT;           // n_top x n_top
   double* fT;                 // scratch n_top
-  int n_tchildren;
-  const long long* tchildren; // [n][2]: bottom node, tmap offset
-  const int* tmap;            // child U position -> top position
+  const int* tptr;            // CSR over top positions: children's cU entries
+  const int* tidx;
   const int* perm;            // natural block -> ND block (restriction / prolongation)
 };
 

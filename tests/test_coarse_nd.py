@@ -49,40 +49,39 @@ def emulate_solve(nd, y):
     """numpy twin of the device solve (coarse.cu) over the packed data; y and
     the result are in ND order."""
     meta = nd.meta.numpy()
-    ch = nd.children.numpy()
-    cmap = nd.cmap.numpy()
-    G, Gt, Z, ZT = nd.G.numpy(), nd.Gt.numpy(), nd.Z.numpy(), nd.ZT.numpy()
+    gmap = nd.gmap.numpy()
+    G, B, ZT = nd.G.numpy(), nd.B.numpy(), nd.ZT.numpy()
     udof = nd.udof.numpy()
     fS = np.zeros(nd.fS.numel())
     cU = np.zeros(nd.cU.numel())
     fwd, bwd = nd.fwd_items.numpy(), nd.bwd_items.numpy()
-    for h in range(nd.H0):  # k_coarse_fwd (or k_coarse_asm + k_coarse_rows)
+
+    def gather(gm, p, base):
+        g = gmap[gm + 2 * p:gm + 2 * p + 2].reshape(-1, 2) if np.ndim(p) == 0 else \
+            np.stack([gmap[gm + 2 * p], gmap[gm + 2 * p + 1]], axis=1)
+        c0 = np.where(g[:, 0] >= 0, cU[np.maximum(g[:, 0], 0)], 0.0)
+        c1 = np.where(g[:, 1] >= 0, cU[np.maximum(g[:, 1], 0)], 0.0)
+        return base + c0 + c1
+
+    for h in range(nd.H0):  # k_coarse_fwd (or k_coarse_asm + assembled rows)
         for node, r0, r1 in fwd[nd.fwd_ptr[h]:nd.fwd_ptr[h + 1]]:
-            s, u, g, z, so, uo, cb, ce = meta[node]
-            f = np.concatenate([y[so:so + s], np.zeros(u)])
-            for k in range(cb, ce):
-                cn, co = ch[k]
-                cu = meta[cn][1]
-                f[cmap[co:co + cu]] += cU[meta[cn][5]:meta[cn][5] + cu]
-            fS[so:so + s] = f[:s]
+            s, u, g, b, so, uo, gm, _ = meta[node]
+            fs = gather(gm, np.arange(s), y[so:so + s])
+            fS[so:so + s] = fs
+            fu = gather(gm, s + np.arange(r0, r1), 0.0)
             Gm = G[g:g + s * u].reshape(u, s)
-            cU[uo + r0:uo + r1] = f[s + r0:s + r1] - Gm[r0:r1] @ f[:s]
+            cU[uo + r0:uo + r1] = fu - Gm[r0:r1] @ fs
     x = np.zeros_like(y)
-    if nd.n_top:  # k_coarse_top_asm + k_coarse_top_rows
+    if nd.n_top:  # k_coarse_top_gather + k_coarse_top_rows
         n = nd.n_top
-        fT = y[nd.top_off:].copy()
-        tch, tmap = nd.tchildren.numpy(), nd.tmap.numpy()
-        for k in range(nd.n_tchildren):
-            cn, to = tch[k]
-            cu = meta[cn][1]
-            fT[tmap[to:to + cu]] += cU[meta[cn][5]:meta[cn][5] + cu]
+        tptr, tidx = nd.tptr.numpy(), nd.tidx.numpy()
+        fT = np.array([y[nd.top_off + i] + cU[tidx[tptr[i]:tptr[i + 1]]].sum() for i in range(n)])
         x[nd.top_off:] = ZT[:n * n].reshape(n, n) @ fT
     for node, r0, r1 in bwd:  # k_coarse_bwd, top-most bottom level first
-        s, u, g, z, so, uo, cb, ce = meta[node]
-        Zm = Z[z:z + s * s].reshape(s, s)
-        Gtm = Gt[g:g + s * u].reshape(s, u)
-        xu = x[udof[uo:uo + u]]
-        x[so + r0:so + r1] = Zm[r0:r1] @ fS[so:so + s] - (Gtm[r0:r1] @ xu if u else 0.0)
+        s, u, g, b, so, uo, gm, _ = meta[node]
+        Bm = B[b:b + s * (s + u)].reshape(s, s + u)
+        v = np.concatenate([fS[so:so + s], x[udof[uo:uo + u]]])
+        x[so + r0:so + r1] = Bm[r0:r1] @ v
     return x
 
 
