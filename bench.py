@@ -278,7 +278,7 @@ def main():
         "clocks": clk.summary(),
     }
     if rank == 0 and not args.no_secondary:
-        line["secondary"] = secondary_solves(tv, fea, torch)
+        line["secondary"] = secondary_solves(tv, fea, torch, p64, hbm)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_matvec(occ, u)
@@ -297,7 +297,27 @@ def _case(tv, d, lo=None, hi=None):
                        loads=loads)
 
 
-def secondary_solves(tv, fea, torch):
+def dpcg_roofline(d, defl, us_per_iter, p64, hbm):
+    """Roofline of one deflated-PCG iteration: the sum of each
+    stage's algorithmic minimum time --
+      2 matvecs (q = A p, t = A z)   each max(1152 Ne flops / P64, 8 (6 Nn + Ne) B / HBM)
+      fused update x, r, z + dots    8 vectors x 8*3Nn B / HBM
+      restriction W^T (t + beta q)   2 vectors / HBM
+      coarse solve                   factor bytes (G, [Z|-G^T], top inverse) / HBM
+      prolongation p = z + beta p - W nu   3 vectors / HBM
+    -- against the measured time per iteration."""
+    vec = 8.0 * d.n_dofs
+    t_mv = max(1152.0 * d.n_elems / (p64 * 1e12), 8.0 * (2 * d.n_dofs + d.n_elems) / (hbm * 1e9))
+    coarse_bytes = float(defl.nd.bytes) if defl.nd is not None else 8.0 * defl.n_vectors ** 2
+    stages = {"matvec_x2": 2 * t_mv, "update": 8 * vec / (hbm * 1e9), "restrict": 2 * vec / (hbm * 1e9),
+              "coarse": coarse_bytes / (hbm * 1e9), "prolong": 3 * vec / (hbm * 1e9)}
+    t_star = sum(stages.values())
+    return {"t_star_us": t_star * 1e6, "frac": t_star * 1e6 / us_per_iter,
+            "stages_us": {k: round(v * 1e6, 2) for k, v in stages.items()},
+            "p64_tflops": p64, "hbm_gbs": hbm}
+
+
+def secondary_solves(tv, fea, torch, p64, hbm):
     """Deflated PCG solves (device-timed): C1, the C4 geometry (north-star target)
     and C2(b) (BASELINE configs[1] part b; infeasible for the reference)."""
     out = {}
@@ -332,10 +352,12 @@ def secondary_solves(tv, fea, torch):
             e.record()
             torch.cuda.synchronize()
             ms = a.elapsed_time(e)
-            out[name] = {"iterations": r.iterations, "solve_ms": ms, "us_per_iter": 1e3 * ms / max(r.iterations, 1),
+            us_it = 1e3 * ms / max(r.iterations, 1)
+            out[name] = {"iterations": r.iterations, "solve_ms": ms, "us_per_iter": us_it,
                          "setup_s": setup, "residual": r.residual, "J": float(fd @ r.u),
                          "n_coarse": defl.n_vectors,
-                         "coarse": "nested dissection" if defl.nd is not None else "dense inverse"}
+                         "coarse": "nested dissection" if defl.nd is not None else "dense inverse",
+                         "roofline": dpcg_roofline(d, defl, us_it, p64, hbm)}
             del op, defl, r
             torch.cuda.empty_cache()
         except Exception as exc:

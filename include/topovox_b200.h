@@ -151,6 +151,13 @@ typedef struct tvb_coarse_nd {
   const int* d_tptr;        /* CSR over top positions of children's update-vector entries */
   const int* d_tidx;
   const int* d_perm;        /* i32[Nb]: natural block -> ND block */
+  /* persistent dataflow schedule (one launch per solve); d_items = NULL -> one launch per level */
+  const int* d_items;       /* [n_items][12] type, wpr, node, r0, r1, wait_idx, wait_need, done_idx, done_need,
+                               rel_begin, rel_end, 0 -- topological order */
+  int n_items;
+  const int* d_rel;
+  unsigned long long* d_cnt;  /* dependency counters, zero-initialised once */
+  unsigned long long* d_ctl;  /* [3] next item, CTAs exited, epoch; zero-initialised once */
   const double* d_factor;   /* the single allocation holding G, B, ZT (L2 persistence window) */
   size_t factor_bytes;
 } tvb_coarse_nd;

@@ -33,6 +33,7 @@ class CoarseND(ctypes.Structure):
         ("n_top", c_int), ("top_off", ctypes.c_longlong), ("top_wpr", c_int),
         ("d_ZT", P), ("d_fT", P), ("d_tptr", P), ("d_tidx", P),
         ("d_perm", P),
+        ("d_items", P), ("n_items", c_int), ("d_rel", P), ("d_cnt", P), ("d_ctl", P),
         ("d_factor", P), ("factor_bytes", c_size_t),
     ]
 

@@ -51,10 +51,21 @@ SPLIT_FRONT = int(os.environ.get("TVB_ND_SPLIT_FRONT", "2048"))
 #: largest top set inverted densely (DOFs); the top tree levels it replaces
 #: would otherwise cost two latency-bound launches each
 TOP_MAX = int(os.environ.get("TVB_ND_TOP_MAX", "4608"))
+#: 1 = one persistent dataflow launch per solve, 0 = one launch per tree level
+#: (default: measured 10-20 % faster at C3/C4a/C5 -- inside a CUDA graph the
+#: per-level launch gap is smaller than the dataflow items' counter traffic)
+FLOW = os.environ.get("TVB_ND_FLOW", "0") != "0"
 #: target warps per solve launch (148 SMs x 16)
 WARPS_IN_FLIGHT = int(os.environ.get("TVB_ND_WARPS", "2368"))
 #: dynamic shared memory per CTA (B200: 227 KB opt-in)
 SMEM_MAX = 227 * 1024
+#: resident 256-thread CTAs on the GPU (148 SMs x 8): one wave of solve items
+CTA_SLOTS = int(os.environ.get("TVB_ND_SLOTS", "1184"))
+
+
+def mode_step(mode: int) -> int:
+    """rows per work item for a row schedule ``mode`` = WPR | RPW << 4."""
+    return 8 * max(1, mode >> 4) // (mode & 15)
 
 
 @dataclass
@@ -153,6 +164,17 @@ class NDCoarseSolver:
         self.n_top = 6 * int(sum(nodes[i].sep.size for i in top))
         self.top_off = 6 * nb - self.n_top
         bidx = {ni: k for k, ni in enumerate(bottom)}
+        # bottom-tree links for the dataflow schedule
+        self._bparent = np.full(len(bottom), -1, dtype=np.int64)     # bottom parent (-1: top parent / root)
+        self._bkids = [[] for _ in bottom]
+        self._top_parent = np.zeros(len(bottom), dtype=bool)
+        for k, ni in enumerate(bottom):
+            p = nodes[ni].parent
+            if p >= 0 and nodes[p].height < self.H0:
+                self._bparent[k] = bidx[p]
+                self._bkids[bidx[p]].append(k)
+            elif p >= 0:
+                self._top_parent[k] = True
         self._factor(torch, Es, nodes, bottom, top, bidx, perm)
         self._make = make_desc
         self.desc = self._make_desc() if make_desc else None
@@ -281,6 +303,24 @@ class NDCoarseSolver:
             w *= 2
         return w
 
+    @classmethod
+    def _mode(cls, rowlen: int, rows_per_node: np.ndarray) -> int:
+        """Row schedule of one launch (coarse.cu ``mode``: WPR | RPW << 4).
+        WPR > 1 splits long rows over warps; with WPR = 1 a warp takes RPW = 2
+        or 4 rows when that brings the launch down to about one wave of CTAs
+        (the per-CTA front/vector load is then amortised over more rows)."""
+        w = cls._wpr(rowlen, int(rows_per_node.sum()))
+        if w > 1:
+            return w
+        forced = os.environ.get("TVB_ND_RPW")
+        if forced:
+            r = int(forced)
+            return 1 if r <= 1 else 1 | (r << 4)
+        rpw = 1
+        while rpw < 4 and int(np.ceil(rows_per_node / (8 * rpw)).sum()) > CTA_SLOTS:
+            rpw *= 2
+        return 1 if rpw == 1 else 1 | (rpw << 4)
+
     def _pack(self, torch, dev, G_list, B_list, s, u, sd, udof_list, gmaps, t_pos, t_idx, n_cu, heights):
         nbot = len(G_list)
         self.n_bottom = nbot
@@ -339,23 +379,25 @@ class NDCoarseSolver:
         fwd, bwd, fptr, bptr, fw, bw = [], [], [0], [0], [], []
         for h in range(self.H0):
             at = np.flatnonzero(heights == h)
-            w = self._wpr(int(s[at].max()) if at.size else 1, int(u[at].sum()))
+            w = self._mode(int(s[at].max()) if at.size else 1, u[at])
             fw.append(w)
+            step = mode_step(w)
             for ni in at:
                 nr = int(u[ni])
-                for r0 in range(0, max(nr, 1), 8 // w):
-                    fwd.append((ni, r0, min(nr, r0 + 8 // w)))
+                for r0 in range(0, max(nr, 1), step):
+                    fwd.append((ni, r0, min(nr, r0 + step)))
             fptr.append(len(fwd))
         for h in range(self.H0 - 1, -1, -1):
             at = np.flatnonzero(heights == h)
-            w = self._wpr(int((s[at] + u[at]).max()) if at.size else 1, int(s[at].sum()))
+            w = self._mode(int((s[at] + u[at]).max()) if at.size else 1, s[at])
             bw.append(w)
+            step = mode_step(w)
             for ni in at:
                 nr = int(s[ni])
-                for r0 in range(0, nr, 8 // w):
-                    bwd.append((ni, r0, min(nr, r0 + 8 // w)))
+                for r0 in range(0, nr, step):
+                    bwd.append((ni, r0, min(nr, r0 + step)))
             bptr.append(len(bwd))
-        self.top_wpr = self._wpr(self.n_top, self.n_top)
+        self.top_wpr = self._mode(self.n_top, np.array([self.n_top]))
         self.fwd_items = torch.from_numpy(np.array(fwd or [(0, 0, 0)], dtype=np.int32).reshape(-1, 3)).to(dev)
         self.bwd_items = torch.from_numpy(np.array(bwd or [(0, 0, 0)], dtype=np.int32).reshape(-1, 3)).to(dev)
         self.fwd_ptr = np.array(fptr, dtype=np.int64)
@@ -375,6 +417,79 @@ class NDCoarseSolver:
         self.asm_nodes = torch.from_numpy(np.array(asm or [0], dtype=np.int32)).to(dev)
         self.asm_ptr = np.array(aptr, dtype=np.int64)
         self.bytes = self.factor.numel() * 8
+        items, rel, ncnt = self._flow_items(s, u, heights)
+        self.n_items = len(items) // 12
+        self.items = torch.from_numpy(np.array(items, dtype=np.int32).reshape(-1, 12)).to(dev)
+        self.rel = torch.from_numpy(np.array(rel + [0], dtype=np.int32)).to(dev)
+        self.cnt = torch.zeros(ncnt + 1, dtype=torch.int64, device=dev)
+        self.ctl = torch.zeros(4, dtype=torch.int64, device=dev)
+
+    # item types of the dataflow schedule (coarse.cu: CoarseItem)
+    FWD, ASM, ROWS, TOP_GATHER, TOP_ROWS, BWD = range(6)
+
+    def _flow_items(self, s, u, heights):
+        """Work items of the persistent dataflow solve in topological order.
+
+        Counters (one int64 each): per bottom node k: fwd_ready[k] (children
+        finished), fwd_done[k], asm_done[k], bwd_ready[k] (parent finished),
+        bwd_done[k]; then top_ready, gather_done, top_done. An item waits for
+        cnt[wait] >= epoch * need and bumps cnt[done]; the item that brings
+        cnt[done] to epoch * need releases its dependants (bumps ``rel``)."""
+        nb = self.n_bottom
+        F_READY, F_DONE, A_DONE, B_READY, B_DONE = (k * nb for k in range(5))
+        TOP_READY, G_DONE, T_DONE = 5 * nb, 5 * nb + 1, 5 * nb + 2
+        items, rel = [], []
+        tchildren = [k for k in range(nb) if self._top_parent[k]]
+
+        def add(typ, wpr, node, r0, r1, wait, wneed, done, dneed, releases):
+            items.extend([typ, wpr, node, r0, r1, wait, wneed, done, dneed, len(rel), len(rel) + len(releases), 0])
+            rel.extend(releases)
+
+        def fwd_release(k):
+            if self._bparent[k] >= 0:
+                return [F_READY + int(self._bparent[k])]
+            if self._top_parent[k]:
+                return [TOP_READY]
+            return [B_READY + k]  # root of a pure-ND tree: its own backward pass may start
+
+        for h in range(self.H0):
+            at = np.flatnonzero(heights == h)
+            w = int(self.fwd_wpr[h])
+            split = bool(self.split[h])
+            step = mode_step(w)
+            for k in at if split else []:
+                nk = len(self._bkids[k])
+                add(self.ASM, 1, k, 0, 0, F_READY + k if nk else -1, nk, A_DONE + k, 1, [])
+            for k in at:
+                nr = int(u[k])
+                chunks = list(range(0, max(nr, 1), step))
+                nk = len(self._bkids[k])
+                wait, wneed = (A_DONE + k, 1) if split else ((F_READY + k, nk) if nk else (-1, 0))
+                rl = fwd_release(k)
+                for r0 in chunks:
+                    add(self.ROWS if split else self.FWD, w, k, r0, min(nr, r0 + step), wait, wneed,
+                        F_DONE + k, len(chunks), rl)
+        if self.n_top:
+            n_g = (self.n_top + 255) // 256
+            for c in range(n_g):
+                add(self.TOP_GATHER, 1, 0, 256 * c, min(self.n_top, 256 * (c + 1)),
+                    TOP_READY if tchildren else -1, len(tchildren), G_DONE, n_g, [])
+            step = mode_step(self.top_wpr)
+            chunks = list(range(0, self.n_top, step))
+            for r0 in chunks:
+                add(self.TOP_ROWS, self.top_wpr, 0, r0, min(self.n_top, r0 + step), G_DONE, n_g, T_DONE,
+                    len(chunks), [B_READY + k for k in tchildren])
+        for gi, h in enumerate(range(self.H0 - 1, -1, -1)):
+            at = np.flatnonzero(heights == h)
+            w = int(self.bwd_wpr[gi])
+            step = mode_step(w)
+            for k in at:
+                nr = int(s[k])
+                chunks = list(range(0, nr, step))
+                for r0 in chunks:
+                    add(self.BWD, w, k, r0, min(nr, r0 + step), B_READY + k, 1, B_DONE + k, len(chunks),
+                        [B_READY + c for c in self._bkids[k]])
+        return items, rel, 5 * nb + 3
 
     def _host_array(self, ctype, values):
         arr = (ctype * len(values))(*values)
@@ -403,6 +518,9 @@ class NDCoarseSolver:
         d.d_ZT, d.d_fT = ptr(self.ZT), ptr(self.fT)
         d.d_tptr, d.d_tidx = ptr(self.tptr), ptr(self.tidx)
         d.d_perm = ptr(self.perm)
+        if FLOW:
+            d.d_items, d.n_items, d.d_rel = ptr(self.items), self.n_items, ptr(self.rel)
+            d.d_cnt, d.d_ctl = ptr(self.cnt), ptr(self.ctl)
         d.d_factor, d.factor_bytes = ptr(self.factor), self.bytes
         return d
 

@@ -133,6 +133,11 @@ static CoarseNDDev coarse_nd_dev(const tvb_coarse_nd* d) {
   D.tptr = d->d_tptr;
   D.tidx = d->d_tidx;
   D.perm = d->d_perm;
+  D.items = d->d_items;
+  D.n_items = d->n_items;
+  D.rel = d->d_rel;
+  D.cnt = d->d_cnt;
+  D.ctl = d->d_ctl;
   return D;
 }
 

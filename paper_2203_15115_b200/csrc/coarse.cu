@@ -11,18 +11,27 @@
 // Top set T (heights >= H0): x_T = S_T^-1 (y_T + sum_children c_child|T).
 //
 // The solve is latency-bound (12k-200k coarse DOFs, a few MB of factor per
-// level), so the kernels are built for short dependency chains:
+// level), so it is built for short dependency chains:
 //   * front vectors are GATHERED: each front position lists the update-vector
 //     entries of (at most two) children, so assembly has no barriers, atomics
 //     or serial child loops (the fixed child order keeps it deterministic);
-//   * one launch per bottom height and direction (plus a per-node assembly
-//     launch for heights with fronts > TVB_ND_SPLIT_FRONT) and two for the top;
-//   * work items are (node, row chunk) pairs, one 256-thread CTA each; long
-//     rows are split across WPR = 1/2/4/8 warps (8/WPR rows per CTA), every
-//     warp a fixed-order lane-strided dot product + shuffle tree, the WPR
-//     parts summed in order through shared memory.
-// Bitwise reproducible run to run.
+//   * work items are (node, row chunk) pairs for one 256-thread CTA; long rows
+//     are split across WPR = 1/2/4/8 warps (8/WPR rows per CTA), every warp a
+//     fixed-order lane-strided dot product + shuffle tree, the WPR parts summed
+//     in order through shared memory;
+//   * default schedule = ONE persistent dataflow kernel (k_coarse_flow): CTAs
+//     pull items in topological order from an atomic counter; each item waits
+//     (acquire) on one counter -- its children finished (forward), its parent
+//     finished (backward) -- and on completion bumps its node's counter, the
+//     last finisher releasing the dependants. No grid-wide barrier and no
+//     launch gap between tree levels; an item only ever waits on items with a
+//     smaller index, all of which are held by running CTAs, so it cannot
+//     deadlock. Counters are epoch-based (never reset).
+//   * fallback schedule (items == nullptr): one launch per tree level.
+// Bitwise reproducible run to run (the arithmetic of an item does not depend
+// on which CTA runs it or when).
 #include <algorithm>
+#include <cstdio>
 
 #include "coarse.cuh"
 
@@ -30,6 +39,8 @@ namespace tvb {
 
 constexpr int kCoarseThreads = 256;
 constexpr int kCoarseWarps = kCoarseThreads / 32;
+
+enum CoarseItem : int { kFwd = 0, kAsm = 1, kRows = 2, kTopGather = 3, kTopRows = 4, kBwd = 5 };
 
 // Part `part` of row . vector (lane-strided over WPR warps), row streamed from
 // global memory with 8 independent loads in flight per lane.
@@ -60,152 +71,317 @@ __device__ __forceinline__ double part_dot(const double* __restrict__ a, const d
   return warp_sum((s0 + s1) + (s2 + s3));
 }
 
-// Rows r0 .. r0+8/WPR-1 (< r1) of M (row length n) dotted with the shared
-// vector v. Returns the full dot to threads t < 8/WPR (row r0 + t).
-template <int WPR>
+// RPW rows at once by one warp (WPR = 1): 8 loads in flight per lane split
+// over the rows. out[q] = row q . b (full warp sum).
+template <int RPW>
+__device__ __forceinline__ void multi_dot(const double* __restrict__ a, long long n, const double* b, int lane,
+                                          double* out) {
+  constexpr int K = 8 / RPW;
+  double s[RPW][2];
+#pragma unroll
+  for (int q = 0; q < RPW; ++q) s[q][0] = s[q][1] = 0.0;
+  int i = lane;
+  for (; i + (K - 1) * 32 < n; i += K * 32) {
+    double w[RPW][K];
+#pragma unroll
+    for (int q = 0; q < RPW; ++q)
+#pragma unroll
+      for (int k = 0; k < K; ++k) w[q][k] = __ldg(a + q * n + i + 32 * k);
+#pragma unroll
+    for (int q = 0; q < RPW; ++q)
+#pragma unroll
+      for (int k = 0; k < K; ++k) s[q][k & 1] = fma(w[q][k], b[i + 32 * k], s[q][k & 1]);
+  }
+  for (; i < n; i += 32)
+#pragma unroll
+    for (int q = 0; q < RPW; ++q) s[q][0] = fma(__ldg(a + q * n + i), b[i], s[q][0]);
+#pragma unroll
+  for (int q = 0; q < RPW; ++q) out[q] = warp_sum(s[q][0] + s[q][1]);
+}
+
+// Rows r0 .. r0 + 8*RPW/WPR - 1 (< r1) of M (row length n) dotted with the
+// shared vector v: WPR warps per row (RPW = 1) or RPW rows per warp (WPR = 1).
+// Returns the full dot to threads t < 8*RPW/WPR (row r0 + t).
+template <int WPR, int RPW>
 __device__ __forceinline__ double rows_dot(const double* __restrict__ M, long long n, const double* v, int r0, int r1,
                                            double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int j = r0 + warp / WPR;
-  const double p = (j < r1) ? part_dot<WPR>(M + (long long)j * n, v, (int)n, warp % WPR, lane) : 0.0;
-  if (lane == 0) red[warp] = p;
+  if (RPW == 1) {
+    const int j = r0 + warp / WPR;
+    const double p = (j < r1) ? part_dot<WPR>(M + (long long)j * n, v, (int)n, warp % WPR, lane) : 0.0;
+    if (lane == 0) red[warp] = p;
+  } else {
+    const int j0 = r0 + warp * RPW;
+    double p[RPW];
+    if (j0 < r1) {
+      // rows past r1 re-read row r1-1 (results discarded)
+      const int jl = min(j0 + RPW, r1) - j0;
+      if (jl == RPW) {
+        multi_dot<RPW>(M + (long long)j0 * n, n, v, lane, p);
+      } else {
+        for (int q = 0; q < RPW; ++q) p[q] = 0.0;
+        for (int q = 0; q < jl; ++q) multi_dot<1>(M + (long long)(j0 + q) * n, n, v, lane, p + q);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < RPW; ++q) p[q] = 0.0;
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < RPW; ++q) red[warp * RPW + q] = p[q];
+  }
   __syncthreads();
   double d = 0.0;
-  if (threadIdx.x < kCoarseWarps / WPR) {
+  if (threadIdx.x < kCoarseWarps * RPW / WPR) {
+    if (RPW == 1) {
 #pragma unroll
-    for (int k = 0; k < WPR; ++k) d += red[threadIdx.x * WPR + k];
+      for (int k = 0; k < WPR; ++k) d += red[threadIdx.x * WPR + k];
+    } else {
+      d = red[threadIdx.x];
+    }
   }
   return d;
 }
 
-// front position p of a node: base + child-0 entry + child-1 entry (fixed order)
+// mode = WPR | RPW << 4 (RPW 0 or 1 = one row per warp)
+__device__ __forceinline__ int mode_rows(int mode) {
+  const int wpr = mode & 15, rpw = max(1, mode >> 4);
+  return kCoarseWarps * rpw / wpr;
+}
+
+__device__ __forceinline__ double rows_dot_w(int mode, const double* __restrict__ M, long long n, const double* v,
+                                             int r0, int r1, double* red) {
+  switch (mode) {
+    case 1: return rows_dot<1, 1>(M, n, v, r0, r1, red);
+    case 2: return rows_dot<2, 1>(M, n, v, r0, r1, red);
+    case 4: return rows_dot<4, 1>(M, n, v, r0, r1, red);
+    case 8: return rows_dot<8, 1>(M, n, v, r0, r1, red);
+    case 1 | (2 << 4): return rows_dot<1, 2>(M, n, v, r0, r1, red);
+    default: return rows_dot<1, 4>(M, n, v, r0, r1, red);
+  }
+}
+
+// front position p of a node: base + child-0 entry + child-1 entry (fixed
+// order). cU is written during the solve: read through L2 (__ldcg).
 __device__ __forceinline__ double gather_front(const CoarseNDDev& D, long long gm, int p, double base) {
   const int g0 = __ldg(D.gmap + gm + 2 * p), g1 = __ldg(D.gmap + gm + 2 * p + 1);
-  if (g0 >= 0) base += D.cU[g0];
-  if (g1 >= 0) base += D.cU[g1];
+  if (g0 >= 0) base += __ldcg(D.cU + g0);
+  if (g1 >= 0) base += __ldcg(D.cU + g1);
   return base;
 }
 
-// Forward rows: c_U[j] = f_U[j] - G[j,:] f_S. ASSEMBLED: f_S / f_U were
-// written by k_coarse_asm (large fronts); else gathered here (and the node's
-// first item stores f_S for the backward pass).
-template <int WPR, bool ASSEMBLED>
-__global__ void __launch_bounds__(kCoarseThreads) k_coarse_fwd(CoarseNDDev D, const int* items, const double* y,
-                                                               const int* stop) {
-  extern __shared__ double fs[];
-  __shared__ double red[kCoarseWarps];
-  if (stop != nullptr && *stop) return;
-  const int* it = items + 3 * blockIdx.x;
-  const int node = it[0], r0 = it[1], r1 = it[2];
+// dst[i] = f(i) for i < n with 8 independent element loads in flight per
+// thread (all loads of a batch are issued before any store).
+template <typename F, typename S>
+__device__ __forceinline__ void batched(int n, F f, S store) {
+  for (int i0 = threadIdx.x; i0 < n; i0 += 8 * blockDim.x) {
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = i0 + k * blockDim.x;
+      v[k] = i < n ? f(i) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = i0 + k * blockDim.x;
+      if (i < n) store(i, v[k]);
+    }
+  }
+}
+
+template <typename F>
+__device__ __forceinline__ void fill_batched(double* dst, int n, F f) {
+  batched(n, f, [&](int i, double v) { dst[i] = v; });
+}
+
+// ---- item bodies (all threads of the CTA; contain __syncthreads) ----------
+
+// Forward rows: c_U[j] = f_U[j] - G[j,:] f_S. assembled: f_S / f_U were written
+// by the node's assembly item; else gathered here (the node's first item
+// also stores f_S for the backward pass).
+__device__ __forceinline__ void item_fwd(const CoarseNDDev& D, bool assembled, int wpr, int node, int r0, int r1,
+                                         const double* y, double* fs, double* red) {
   const long long* m = D.meta + 8 * node;
   const int s = (int)m[0];
   const long long g_off = m[2], sd_off = m[4], ud_off = m[5], gm = m[6];
-  for (int i = threadIdx.x; i < s; i += blockDim.x) {
-    if (ASSEMBLED) {
-      fs[i] = D.fS[sd_off + i];
-    } else {
-      const double v = gather_front(D, gm, i, y[sd_off + i]);
-      fs[i] = v;
-      if (r0 == 0) D.fS[sd_off + i] = v;
-    }
+  if (assembled) {
+    fill_batched(fs, s, [&](int i) { return __ldcg(D.fS + sd_off + i); });
+  } else {
+    fill_batched(fs, s, [&](int i) { return gather_front(D, gm, i, y[sd_off + i]); });
+    if (r0 == 0)
+      for (int i = threadIdx.x; i < s; i += blockDim.x) D.fS[sd_off + i] = fs[i];  // own writes: no barrier
   }
   __syncthreads();
-  const double d = rows_dot<WPR>(D.G + g_off, s, fs, r0, r1, red);
+  const double d = rows_dot_w(wpr, D.G + g_off, s, fs, r0, r1, red);
   const int j = r0 + threadIdx.x;
-  if (threadIdx.x < kCoarseWarps / WPR && j < r1) {
-    const double fu = ASSEMBLED ? D.cU[ud_off + j] : gather_front(D, gm, s + j, 0.0);
+  if (threadIdx.x < mode_rows(wpr) && j < r1) {
+    const double fu = assembled ? __ldcg(D.cU + ud_off + j) : gather_front(D, gm, s + j, 0.0);
     D.cU[ud_off + j] = fu - d;
   }
 }
 
-// Large fronts, assembly pass: f_S -> fS, f_U -> cU (one CTA per node).
-__global__ void __launch_bounds__(kCoarseThreads) k_coarse_asm(CoarseNDDev D, const int* nodes, const double* y,
-                                                               const int* stop) {
-  if (stop != nullptr && *stop) return;
-  const int node = nodes[blockIdx.x];
+// Large fronts, assembly: f_S -> fS, f_U -> cU (whole node).
+__device__ __forceinline__ void item_asm(const CoarseNDDev& D, int node, const double* y) {
   const long long* m = D.meta + 8 * node;
   const int s = (int)m[0], u = (int)m[1];
   const long long sd_off = m[4], ud_off = m[5], gm = m[6];
-  for (int p = threadIdx.x; p < s + u; p += blockDim.x) {
-    if (p < s) D.fS[sd_off + p] = gather_front(D, gm, p, y[sd_off + p]);
-    else D.cU[ud_off + p - s] = gather_front(D, gm, p, 0.0);
-  }
+  batched(
+      s + u, [&](int p) { return gather_front(D, gm, p, p < s ? y[sd_off + p] : 0.0); },
+      [&](int p, double v) {
+        if (p < s) D.fS[sd_off + p] = v;
+        else D.cU[ud_off + p - s] = v;
+      });
 }
 
 // Backward rows: x_S[j] = [Z | -G^T][j,:] . [f_S ; x_U].
-template <int WPR>
-__global__ void __launch_bounds__(kCoarseThreads) k_coarse_bwd(CoarseNDDev D, const int* items, double* x,
-                                                               const int* stop) {
-  extern __shared__ double v[];
-  __shared__ double red[kCoarseWarps];
-  if (stop != nullptr && *stop) return;
-  const int* it = items + 3 * blockIdx.x;
-  const int node = it[0], r0 = it[1], r1 = it[2];
+__device__ __forceinline__ void item_bwd(const CoarseNDDev& D, int wpr, int node, int r0, int r1, double* x,
+                                         double* v, double* red) {
   const long long* m = D.meta + 8 * node;
   const int s = (int)m[0], u = (int)m[1];
   const long long b_off = m[3], sd_off = m[4], ud_off = m[5];
-  for (int i = threadIdx.x; i < s + u; i += blockDim.x)
-    v[i] = i < s ? D.fS[sd_off + i] : x[__ldg(D.udof + ud_off + i - s)];
+  fill_batched(v, s + u, [&](int i) {
+    return i < s ? __ldcg(D.fS + sd_off + i) : __ldcg(x + __ldg(D.udof + ud_off + i - s));
+  });
   __syncthreads();
-  const double d = rows_dot<WPR>(D.B + b_off, s + u, v, r0, r1, red);
+  const double d = rows_dot_w(wpr, D.B + b_off, s + u, v, r0, r1, red);
   const int j = r0 + threadIdx.x;
-  if (threadIdx.x < kCoarseWarps / WPR && j < r1) x[sd_off + j] = d;
+  if (threadIdx.x < mode_rows(wpr) && j < r1) x[sd_off + j] = d;
 }
 
-// Top set, part 1: fT = y_T + children's update entries (CSR, fixed order).
-__global__ void k_coarse_top_gather(CoarseNDDev D, const double* y, const int* stop) {
-  if (stop != nullptr && *stop) return;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= D.n_top) return;
+// Top set, gather: fT[i] = y_T[i] + children's update entries (CSR, fixed order).
+__device__ __forceinline__ void item_top_gather(const CoarseNDDev& D, int i0, int i1, const double* y) {
+  const int i = i0 + threadIdx.x;
+  if (i >= i1) return;
   double v = y[D.top_off + i];
   const int a = __ldg(D.tptr + i), b = __ldg(D.tptr + i + 1);
-  for (int k = a; k < b; ++k) v += D.cU[__ldg(D.tidx + k)];
+  for (int k = a; k < b; ++k) v += __ldcg(D.cU + __ldg(D.tidx + k));
   D.fT[i] = v;
 }
 
-// Top set, part 2: x_T = S_T^-1 fT (dense rows).
-template <int WPR>
-__global__ void __launch_bounds__(kCoarseThreads) k_coarse_top_rows(CoarseNDDev D, double* x, const int* stop) {
-  extern __shared__ double ft[];
-  __shared__ double red[kCoarseWarps];
-  if (stop != nullptr && *stop) return;
+// Top set, rows: x_T = S_T^-1 fT.
+__device__ __forceinline__ void item_top_rows(const CoarseNDDev& D, int wpr, int r0, int r1, double* x, double* ft,
+                                              double* red) {
   const int n = D.n_top;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) ft[i] = D.fT[i];
+  fill_batched(ft, n, [&](int i) { return __ldcg(D.fT + i); });
   __syncthreads();
-  const int r0 = blockIdx.x * (kCoarseWarps / WPR);
-  const int r1 = min(n, r0 + kCoarseWarps / WPR);
-  const double d = rows_dot<WPR>(D.ZT, n, ft, r0, r1, red);
+  const double d = rows_dot_w(wpr, D.ZT, n, ft, r0, r1, red);
   const int j = r0 + threadIdx.x;
-  if (threadIdx.x < kCoarseWarps / WPR && j < r1) x[D.top_off + j] = d;
+  if (threadIdx.x < mode_rows(wpr) && j < r1) x[D.top_off + j] = d;
+}
+
+// ---- persistent dataflow schedule -------------------------------------------
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// item record (12 ints): type, wpr, node, r0, r1, wait_idx, wait_need,
+// done_idx, done_need, rel_begin, rel_end, 0
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_flow(CoarseNDDev D, const double* y, double* x,
+                                                                const int* stop) {
+  extern __shared__ double sm[];
+  __shared__ double red[4 * kCoarseWarps];
+  __shared__ int s_item;
+  if (stop != nullptr && *stop) return;
+  const unsigned long long E = __ldcg(D.ctl + 2) + 1;  // this solve's epoch (1-based)
+  unsigned long long* cnt = D.cnt;
+  while (true) {
+    if (threadIdx.x == 0) s_item = (int)atomicAdd(D.ctl, 1ull);
+    __syncthreads();
+    const int k = s_item;
+    if (k >= D.n_items) break;
+    const int* it = D.items + 12 * k;
+    const int type = it[0], wpr = it[1], node = it[2], r0 = it[3], r1 = it[4];
+    if (threadIdx.x == 0) {
+      const int wi = it[5];
+      if (wi >= 0) {
+        const unsigned long long target = E * (unsigned long long)it[6];
+        unsigned int spins = 0;
+        while (ld_acquire(cnt + wi) < target) {
+          __nanosleep(64);
+          if (++spins == (1u << 26)) {  // several seconds: a broken schedule must fail, not hang
+            printf("k_coarse_flow: item %d stuck on counter %d (%llu < %llu)\n", k, wi, ld_acquire(cnt + wi),
+                   target);
+            __trap();
+          }
+        }
+      }
+    }
+    __syncthreads();
+    switch (type) {
+      case kFwd: item_fwd(D, false, wpr, node, r0, r1, y, sm, red); break;
+      case kAsm: item_asm(D, node, y); break;
+      case kRows: item_fwd(D, true, wpr, node, r0, r1, y, sm, red); break;
+      case kTopGather: item_top_gather(D, r0, r1, y); break;
+      case kTopRows: item_top_rows(D, wpr, r0, r1, x, sm, red); break;
+      default: item_bwd(D, wpr, node, r0, r1, x, sm, red); break;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const unsigned long long old = atomicAdd(cnt + it[7], 1ull);
+      if (old + 1 == E * (unsigned long long)it[8]) {
+        __threadfence();
+        for (int j = it[9]; j < it[10]; ++j) atomicAdd(cnt + __ldg(D.rel + j), 1ull);
+      }
+    }
+  }
+  // last CTA out rewinds the item counter and advances the epoch
+  if (threadIdx.x == 0) {
+    const unsigned long long old = atomicAdd(D.ctl + 1, 1ull);
+    if (old == gridDim.x - 1) {
+      D.ctl[0] = 0ull;
+      D.ctl[1] = 0ull;
+      D.ctl[2] = E;
+      __threadfence();
+    }
+  }
+}
+
+// ---- per-level schedule (fallback) -----------------------------------------
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_fwd(CoarseNDDev D, int wpr, int assembled,
+                                                               const int* items, const double* y, const int* stop) {
+  extern __shared__ double sm[];
+  __shared__ double red[4 * kCoarseWarps];
+  if (stop != nullptr && *stop) return;
+  const int* it = items + 3 * blockIdx.x;
+  item_fwd(D, assembled != 0, wpr, it[0], it[1], it[2], y, sm, red);
+}
+
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_asm(CoarseNDDev D, const int* nodes, const double* y,
+                                                               const int* stop) {
+  if (stop != nullptr && *stop) return;
+  item_asm(D, nodes[blockIdx.x], y);
+}
+
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_bwd(CoarseNDDev D, int wpr, const int* items, double* x,
+                                                               const int* stop) {
+  extern __shared__ double sm[];
+  __shared__ double red[4 * kCoarseWarps];
+  if (stop != nullptr && *stop) return;
+  const int* it = items + 3 * blockIdx.x;
+  item_bwd(D, wpr, it[0], it[1], it[2], x, sm, red);
+}
+
+__global__ void k_coarse_top_gather(CoarseNDDev D, const double* y, const int* stop) {
+  if (stop != nullptr && *stop) return;
+  item_top_gather(D, blockIdx.x * blockDim.x, D.n_top, y);
+}
+
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_top_rows(CoarseNDDev D, double* x, const int* stop) {
+  extern __shared__ double sm[];
+  __shared__ double red[4 * kCoarseWarps];
+  if (stop != nullptr && *stop) return;
+  const int rpc = mode_rows(D.top_wpr);
+  const int r0 = blockIdx.x * rpc;
+  item_top_rows(D, D.top_wpr, r0, min(D.n_top, r0 + rpc), x, sm, red);
 }
 
 template <typename K>
 static void allow_smem(K kernel, int bytes) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
-
-template <int WPR>
-static void set_smem_all(int bytes) {
-  allow_smem(k_coarse_fwd<WPR, false>, bytes);
-  allow_smem(k_coarse_fwd<WPR, true>, bytes);
-  allow_smem(k_coarse_bwd<WPR>, bytes);
-  allow_smem(k_coarse_top_rows<WPR>, bytes);
-}
-
-template <int WPR>
-static void launch_fwd(bool assembled, unsigned n, int smem, const CoarseNDDev& D, const int* items, const double* y,
-                       const int* stop, cudaStream_t s) {
-  if (assembled) k_coarse_fwd<WPR, true><<<n, kCoarseThreads, smem, s>>>(D, items, y, stop);
-  else k_coarse_fwd<WPR, false><<<n, kCoarseThreads, smem, s>>>(D, items, y, stop);
-}
-
-#define TVB_WPR_DISPATCH(w, CALL) \
-  switch (w) {                    \
-    case 1: CALL(1); break;       \
-    case 2: CALL(2); break;       \
-    case 4: CALL(4); break;       \
-    default: CALL(8); break;      \
-  }
 
 cudaError_t launch_coarse_nd(const CoarseNDDev& D, const double* y, double* x, const int* stop, cudaStream_t s) {
   static int attr_max = 0;
@@ -214,39 +390,46 @@ cudaError_t launch_coarse_nd(const CoarseNDDev& D, const double* y, double* x, c
   const int smem_top = (int)(sizeof(double) * (size_t)(D.n_top + 1));
   const int smem_max = std::max(smem_bwd, smem_top);
   if (smem_max > attr_max) {
-    set_smem_all<1>(smem_max);
-    set_smem_all<2>(smem_max);
-    set_smem_all<4>(smem_max);
-    set_smem_all<8>(smem_max);
+    allow_smem(k_coarse_flow, smem_max);
+    allow_smem(k_coarse_fwd, smem_max);
+    allow_smem(k_coarse_bwd, smem_max);
+    allow_smem(k_coarse_top_rows, smem_max);
     attr_max = smem_max;
+  }
+  if (D.items != nullptr && D.n_items > 0) {
+    static int cached_smem = -1, cached_ctas = 0;
+    if (cached_smem != smem_max) {
+      int dev = 0, nsm = 148, per_sm = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_flow, kCoarseThreads, smem_max);
+      cached_ctas = nsm * std::max(1, per_sm);
+      cached_smem = smem_max;
+    }
+    const int ctas = std::min(cached_ctas, D.n_items);
+    k_coarse_flow<<<(unsigned)ctas, kCoarseThreads, smem_max, s>>>(D, y, x, stop);
+    return cudaGetLastError();
   }
   for (int h = 0; h < D.n_levels; ++h) {
     const long long a = D.fwd_ptr[h], b = D.fwd_ptr[h + 1];
     if (b <= a) continue;
-    const bool split = D.split[h] != 0;
+    const int split = D.split[h] != 0;
     if (split) {
       const long long na = D.asm_ptr[h], nb = D.asm_ptr[h + 1];
       k_coarse_asm<<<(unsigned)(nb - na), kCoarseThreads, 0, s>>>(D, D.asm_nodes + na, y, stop);
     }
-#define TVB_FWD(W) launch_fwd<W>(split, (unsigned)(b - a), smem_fwd, D, D.fwd_items + 3 * a, y, stop, s)
-    TVB_WPR_DISPATCH(D.fwd_wpr[h], TVB_FWD)
-#undef TVB_FWD
+    k_coarse_fwd<<<(unsigned)(b - a), kCoarseThreads, smem_fwd, s>>>(D, D.fwd_wpr[h], split, D.fwd_items + 3 * a, y,
+                                                                      stop);
   }
   if (D.n_top > 0) {
     k_coarse_top_gather<<<(unsigned)((D.n_top + 255) / 256), 256, 0, s>>>(D, y, stop);
-#define TVB_TOP(W)                                                                                           \
-  k_coarse_top_rows<W><<<(unsigned)((D.n_top + kCoarseWarps / W - 1) / (kCoarseWarps / W)), kCoarseThreads, \
-                         smem_top, s>>>(D, x, stop)
-    TVB_WPR_DISPATCH(D.top_wpr, TVB_TOP)
-#undef TVB_TOP
+    const int rpc = kCoarseWarps * std::max(1, D.top_wpr >> 4) / (D.top_wpr & 15);
+    k_coarse_top_rows<<<(unsigned)((D.n_top + rpc - 1) / rpc), kCoarseThreads, smem_top, s>>>(D, x, stop);
   }
   for (int h = 0; h < D.n_levels; ++h) {  // bwd groups: top-most bottom level first
     const long long a = D.bwd_ptr[h], b = D.bwd_ptr[h + 1];
-    if (b <= a) continue;
-#define TVB_BWD(W) \
-  k_coarse_bwd<W><<<(unsigned)(b - a), kCoarseThreads, smem_bwd, s>>>(D, D.bwd_items + 3 * a, x, stop)
-    TVB_WPR_DISPATCH(D.bwd_wpr[h], TVB_BWD)
-#undef TVB_BWD
+    if (b > a)
+      k_coarse_bwd<<<(unsigned)(b - a), kCoarseThreads, smem_bwd, s>>>(D, D.bwd_wpr[h], D.bwd_items + 3 * a, x, stop);
   }
   return cudaGetLastError();
 }

@@ -33,6 +33,13 @@ struct CoarseNDDev {
   const int* tptr;            // CSR over top positions: children's cU entries
   const int* tidx;
   const int* perm;            // natural block -> ND block (restriction / prolongation)
+  // persistent dataflow schedule (k_coarse_flow); items == nullptr -> per-level launches
+  const int* items;           // [n_items][12] type, wpr, node, r0, r1, wait_idx, wait_need, done_idx, done_need,
+                              //               rel_begin, rel_end, 0   (topological order)
+  int n_items;
+  const int* rel;             // counters released by a node's last finishing item
+  unsigned long long* cnt;    // dependency counters (epoch-scaled, never reset)
+  unsigned long long* ctl;    // [3]: next item, CTAs exited, epoch
 };
 
 cudaError_t launch_coarse_nd(const CoarseNDDev& D, const double* y, double* x, const int* stop, cudaStream_t s);

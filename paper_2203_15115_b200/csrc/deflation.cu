@@ -7,6 +7,8 @@
 // of the same span. Restriction is then a force/torque moment sum over the
 // block's closed node box followed by S^T; prolongation evaluates the rigid
 // motion t + omega x r of every block containing a node.
+#include <algorithm>
+
 #include "deflation.cuh"
 #include "vec.cuh"
 
@@ -210,10 +212,14 @@ cudaError_t launch_block_basis(const Agglo& A, const double* occ, const uint8_t*
 // ---------------------------------------------------------------------------
 constexpr int kRestrictThreads = 256;
 
-__global__ void __launch_bounds__(kRestrictThreads) k_restrict(Agglo A, const uint8_t* nflags, DeflData D,
-                                                               const double* y, const double* y2,
-                                                               const SolverState* st, double* yc, const int* stop) {
-  __shared__ double red[32], m[6];
+// BS > 0: compile-time block size (the closed box has at most (BS+1)^3 nodes;
+// positions outside a clipped boundary box are skipped); BS = 0: runtime size.
+template <int BS>
+__global__ void __launch_bounds__(kRestrictThreads) k_restrict(Agglo A, const uint8_t* __restrict__ nflags, DeflData D,
+                                                               const double* __restrict__ y,
+                                                               const double* __restrict__ y2, const SolverState* st,
+                                                               double* yc, const int* stop) {
+  __shared__ double red[6 * (kRestrictThreads / 32)], m[6];
   if (stop != nullptr && *stop) return;
   const double beta = (y2 != nullptr) ? st->beta : 0.0;  // restrict y + beta*y2
   const long long B = blockIdx.x;
@@ -228,36 +234,67 @@ __global__ void __launch_bounds__(kRestrictThreads) k_restrict(Agglo A, const ui
   const Grid& G = A.g;
   const int X0 = A.b * bx, Y0 = A.b * by, Z0 = A.b * bz;
   const double cx = D.cen[3 * B], cy = D.cen[3 * B + 1], cz = D.cen[3 * B + 2];
-  const int nnl = nxl * nyl * nzl;
+  const int PX = BS > 0 ? BS + 1 : nxl, PY = BS > 0 ? BS + 1 : nyl, PZ = BS > 0 ? BS + 1 : nzl;
+  const int npos = PX * PY * PZ;
   double acc[6] = {0, 0, 0, 0, 0, 0};
-  for (int i = threadIdx.x; i < nnl; i += blockDim.x) {
-    const int lx = i % nxl, ly = (i / nxl) % nyl, lz = i / (nxl * nyl);
-    const long long n = G.node(X0 + lx, Y0 + ly, Z0 + lz);
-    // independent loads (flags and all three components in flight together)
-    const uint8_t fl = __ldg(nflags + n);
-    double w0 = __ldg(y + 3 * n), w1 = __ldg(y + 3 * n + 1), w2 = __ldg(y + 3 * n + 2);
-    if (y2 != nullptr) {
-      w0 = fma(beta, __ldg(y2 + 3 * n), w0);
-      w1 = fma(beta, __ldg(y2 + 3 * n + 1), w1);
-      w2 = fma(beta, __ldg(y2 + 3 * n + 2), w2);
+  // up to kNodes nodes per thread per step, all their loads issued before use
+  constexpr int kNodes = 3;
+  for (int i0 = threadIdx.x; i0 < npos; i0 += kNodes * blockDim.x) {
+    uint8_t fl[kNodes];
+    double w[kNodes][3];
+    int lxs[kNodes], lys[kNodes], lzs[kNodes];
+#pragma unroll
+    for (int k = 0; k < kNodes; ++k) {
+      const int i = i0 + k * blockDim.x;
+      const int lx = i % PX, ly = (i / PX) % PY, lz = i / (PX * PY);
+      lxs[k] = lx;
+      lys[k] = ly;
+      lzs[k] = lz;
+      fl[k] = 0;
+      w[k][0] = w[k][1] = w[k][2] = 0.0;
+      if (i < npos && lx < nxl && ly < nyl && lz < nzl) {
+        const long long n = G.node(X0 + lx, Y0 + ly, Z0 + lz);
+        fl[k] = __ldg(nflags + n);
+        w[k][0] = __ldg(y + 3 * n);
+        w[k][1] = __ldg(y + 3 * n + 1);
+        w[k][2] = __ldg(y + 3 * n + 2);
+        if (y2 != nullptr) {
+          w[k][0] = fma(beta, __ldg(y2 + 3 * n), w[k][0]);
+          w[k][1] = fma(beta, __ldg(y2 + 3 * n + 1), w[k][1]);
+          w[k][2] = fma(beta, __ldg(y2 + 3 * n + 2), w[k][2]);
+        }
+      }
     }
-    if (!(fl & kStructBit)) continue;
-    const double vx = (fl & 1) ? 0.0 : w0;
-    const double vy = (fl & 2) ? 0.0 : w1;
-    const double vz = (fl & 4) ? 0.0 : w2;
-    const double rx = A.h * (lx - cx), ry = A.h * (ly - cy), rz = A.h * (lz - cz);
-    acc[0] += vx;
-    acc[1] += vy;
-    acc[2] += vz;
-    acc[3] += ry * vz - rz * vy;
-    acc[4] += rz * vx - rx * vz;
-    acc[5] += rx * vy - ry * vx;
+#pragma unroll
+    for (int k = 0; k < kNodes; ++k) {
+      if (!(fl[k] & kStructBit)) continue;  // also covers positions outside the box (fl = 0)
+      const double vx = (fl[k] & 1) ? 0.0 : w[k][0];
+      const double vy = (fl[k] & 2) ? 0.0 : w[k][1];
+      const double vz = (fl[k] & 4) ? 0.0 : w[k][2];
+      const double rx = A.h * (lxs[k] - cx), ry = A.h * (lys[k] - cy), rz = A.h * (lzs[k] - cz);
+      acc[0] += vx;
+      acc[1] += vy;
+      acc[2] += vz;
+      acc[3] += ry * vz - rz * vy;
+      acc[4] += rz * vx - rx * vz;
+      acc[5] += rx * vy - ry * vx;
+    }
   }
+  // the six moment sums reduced together: warp trees, then 6 threads sum the
+  // per-warp values in warp order (one barrier)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
   for (int k = 0; k < 6; ++k) {
-    const double s = block_sum(acc[k], red);
-    if (threadIdx.x == 0) m[k] = s;
+    const double s = warp_sum(acc[k]);
+    if (lane == 0) red[6 * wid + k] = s;
   }
   __syncthreads();
+  if (threadIdx.x < 6) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[6 * w + threadIdx.x];
+    m[threadIdx.x] = s;
+  }
+  __syncwarp();
   if (threadIdx.x < 6) {
     const int j = threadIdx.x;
     const double* S = D.S + 36 * B;
@@ -269,7 +306,11 @@ __global__ void __launch_bounds__(kRestrictThreads) k_restrict(Agglo A, const ui
 
 cudaError_t launch_restrict(const Agglo& A, const uint8_t* nflags, DeflData D, const double* y, double* yc,
                             cudaStream_t s, const int* stop, const double* y2, const void* state) {
-  k_restrict<<<(unsigned)A.nb, kRestrictThreads, 0, s>>>(A, nflags, D, y, y2, (const SolverState*)state, yc, stop);
+  const SolverState* st = (const SolverState*)state;
+  const unsigned g = (unsigned)A.nb;
+  if (A.b == 8) k_restrict<8><<<g, kRestrictThreads, 0, s>>>(A, nflags, D, y, y2, st, yc, stop);
+  else if (A.b == 4) k_restrict<4><<<g, kRestrictThreads, 0, s>>>(A, nflags, D, y, y2, st, yc, stop);
+  else k_restrict<0><<<g, kRestrictThreads, 0, s>>>(A, nflags, D, y, y2, st, yc, stop);
   return cudaGetLastError();
 }
 
@@ -296,17 +337,35 @@ cudaError_t launch_block_nu(const Agglo& A, DeflData D, const double* mu, double
 // ---------------------------------------------------------------------------
 // prolongation: (W mu)_n = sum_{B containing n} mask(t_B + omega_B x r_{n,B})
 // ---------------------------------------------------------------------------
-__global__ void k_prolong(Agglo A, const uint8_t* nflags, const double* cen, const int* keepv, const double* nu,
-                          double* out, const double* z, const SolverState* st, int mode) {
-  const long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+// One thread per node (1-D grid, 32-bit index math: Nn < 2^31). All loads of
+// the node (flags, p, z) are issued before the rigid-motion evaluation.
+// BS > 0: compile-time block size (divisions by BS become shifts / mul-hi).
+template <int BS>
+__global__ void __launch_bounds__(256) k_prolong(Agglo A, const uint8_t* __restrict__ nflags,
+                                                 const double* __restrict__ cen, const double* __restrict__ nu,
+                                                 double* __restrict__ out, const double* __restrict__ z,
+                                                 const SolverState* st, int mode) {
   const Grid& G = A.g;
-  if (n >= G.nn) return;
+  const unsigned n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= (unsigned)G.nn) return;
   if (st != nullptr && st->done) return;
   const uint8_t fl = nflags[n];
+  double o[3] = {0.0, 0.0, 0.0}, zv[3] = {0.0, 0.0, 0.0};
+  if (mode != 0) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) zv[a] = z[3ull * n + a];
+  }
+  if (mode == 1) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) o[a] = out[3ull * n + a];
+  }
   double v[3] = {0.0, 0.0, 0.0};
   if (fl & kStructBit) {
-    const int x = (int)(n % G.px), y = (int)((n / G.px) % G.py), zz = (int)(n / ((long long)G.px * G.py));
-    const int b = A.b;
+    const unsigned px = (unsigned)G.px, py = (unsigned)G.py;
+    const unsigned t = n / px;
+    const unsigned zu = t / py;
+    const int x = (int)(n - t * px), y = (int)(t - zu * py), zz = (int)zu;
+    const int b = BS > 0 ? BS : A.b;
     int bxs[2], bys[2], bzs[2], nbx = 0, nby = 0, nbz = 0;
     // blocks whose closed box contains the coordinate, ascending
     if (x % b == 0 && x > 0 && x / b - 1 < A.mx) bxs[nbx++] = x / b - 1;
@@ -331,20 +390,21 @@ __global__ void k_prolong(Agglo A, const uint8_t* nflags, const double* cen, con
     for (int a = 0; a < 3; ++a)
       if ((fl >> a) & 1) v[a] = 0.0;
   }
-  if (mode == 0) {
-    for (int a = 0; a < 3; ++a) out[3 * n + a] = v[a];
-  } else if (mode == 1) {
-    const double beta = st->beta;
-    for (int a = 0; a < 3; ++a) out[3 * n + a] = fma(beta, out[3 * n + a], z[3 * n + a]) - v[a];
-  } else {
-    for (int a = 0; a < 3; ++a) out[3 * n + a] = z[3 * n + a] - v[a];
+  const double beta = mode == 1 ? st->beta : 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double r = mode == 0 ? v[a] : (mode == 1 ? fma(beta, o[a], zv[a]) - v[a] : zv[a] - v[a]);
+    out[3ull * n + a] = r;
   }
 }
 
 cudaError_t launch_prolong(const Agglo& A, const uint8_t* nflags, DeflData D, const double* nu, double* out,
                            const double* z, const void* state, int mode, cudaStream_t s) {
-  k_prolong<<<(unsigned)((A.g.nn + 255) / 256), 256, 0, s>>>(A, nflags, D.cen, D.keep, nu, out, z,
-                                                              (const SolverState*)state, mode);
+  const unsigned g = (unsigned)((A.g.nn + 255) / 256);
+  const SolverState* st = (const SolverState*)state;
+  if (A.b == 8) k_prolong<8><<<g, 256, 0, s>>>(A, nflags, D.cen, nu, out, z, st, mode);
+  else if (A.b == 4) k_prolong<4><<<g, 256, 0, s>>>(A, nflags, D.cen, nu, out, z, st, mode);
+  else k_prolong<0><<<g, 256, 0, s>>>(A, nflags, D.cen, nu, out, z, st, mode);
   return cudaGetLastError();
 }
 

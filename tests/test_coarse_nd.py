@@ -111,3 +111,89 @@ def test_nd_factor_matches_dense(grid, leaf, top_max):
     x = emulate_solve(nd, yn)[ndi]
     ref = np.linalg.solve(E, y)
     assert np.abs(x - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def run_flow(nd, y, epochs=2, workers=7, seed=0):
+    """numpy twin of k_coarse_flow: `workers` persistent CTAs pull items in
+    index order and finish them in random order once their dependency counter
+    is satisfied; checks the schedule never deadlocks over several epochs."""
+    rng = np.random.default_rng(seed)
+    meta = nd.meta.numpy()
+    gmap = nd.gmap.numpy()
+    G, B, ZT = nd.G.numpy(), nd.B.numpy(), nd.ZT.numpy()
+    udof, items, rel = nd.udof.numpy(), nd.items.numpy(), nd.rel.numpy()
+    tptr, tidx = nd.tptr.numpy(), nd.tidx.numpy()
+    cnt = np.zeros(nd.cnt.numel(), dtype=np.int64)
+
+    def gather(gm, p, base):
+        c0 = np.where(gmap[gm + 2 * p] >= 0, cU[np.maximum(gmap[gm + 2 * p], 0)], 0.0)
+        c1 = np.where(gmap[gm + 2 * p + 1] >= 0, cU[np.maximum(gmap[gm + 2 * p + 1], 0)], 0.0)
+        return base + c0 + c1
+
+    for E in range(1, epochs + 1):
+        fS = np.full(nd.fS.numel(), np.nan)
+        cU = np.full(nd.cU.numel(), np.nan)
+        fT = np.full(nd.fT.numel(), np.nan)
+        x = np.full_like(y, np.nan)
+        nxt, running = 0, []
+        while nxt < len(items) or running:
+            while len(running) < workers and nxt < len(items):
+                running.append(nxt)
+                nxt += 1
+            ready = [k for k in running if items[k][5] < 0 or cnt[items[k][5]] >= E * items[k][6]]
+            assert ready, "dataflow schedule deadlocked"
+            k = ready[rng.integers(len(ready))]
+            running.remove(k)
+            typ, wpr, node, r0, r1 = items[k][:5]
+            if typ in (0, 1, 2):
+                s, u, g, b, so, uo, gm, _ = meta[node]
+                if typ == 1:
+                    fS[so:so + s] = gather(gm, np.arange(s), y[so:so + s])
+                    cU[uo:uo + u] = gather(gm, s + np.arange(u), 0.0)
+                else:
+                    if typ == 0:
+                        fs = gather(gm, np.arange(s), y[so:so + s])
+                        if r0 == 0:
+                            fS[so:so + s] = fs
+                        fu = gather(gm, s + np.arange(r0, r1), 0.0)
+                    else:
+                        fs = fS[so:so + s]
+                        fu = cU[uo + r0:uo + r1]
+                    assert np.isfinite(fs).all() and np.isfinite(fu).all()
+                    cU[uo + r0:uo + r1] = fu - G[g:g + s * u].reshape(u, s)[r0:r1] @ fs
+            elif typ == 3:
+                for i in range(r0, r1):
+                    fT[i] = y[nd.top_off + i] + cU[tidx[tptr[i]:tptr[i + 1]]].sum()
+            elif typ == 4:
+                n = nd.n_top
+                assert np.isfinite(fT[:n]).all()
+                x[nd.top_off + r0:nd.top_off + r1] = ZT[:n * n].reshape(n, n)[r0:r1] @ fT[:n]
+            else:
+                s, u, g, b, so, uo, gm, _ = meta[node]
+                v = np.concatenate([fS[so:so + s], x[udof[uo:uo + u]]])
+                assert np.isfinite(v).all()
+                x[so + r0:so + r1] = B[b:b + s * (s + u)].reshape(s, s + u)[r0:r1] @ v
+            cnt[items[k][7]] += 1
+            if cnt[items[k][7]] == E * items[k][8]:
+                for j in range(items[k][9], items[k][10]):
+                    cnt[rel[j]] += 1
+    return x
+
+
+@pytest.mark.parametrize("top_max", [0, 60, 4608])
+@pytest.mark.parametrize("grid,leaf", [((5, 5, 10), 27), ((4, 3, 2), 2), ((9, 8, 7), 8), ((1, 1, 1), 27)])
+def test_nd_dataflow_schedule(grid, leaf, top_max, monkeypatch):
+    import paper_2203_15115_b200.coarse as C
+
+    monkeypatch.setattr(C, "SPLIT_FRONT", 200)  # exercise the assembly items too
+    mx, my, mz = grid
+    Es = random_block_stencil(mx, my, mz, seed=sum(grid) + 1)
+    E = dense_of(Es, mx, my, mz)
+    nd = C.NDCoarseSolver(grid, torch.from_numpy(Es.reshape(-1)), leaf_max=leaf, top_max=top_max, make_desc=False)
+    y = np.random.default_rng(3).standard_normal(E.shape[0])
+    ndi = nd.nd_index()
+    yn = np.empty_like(y)
+    yn[ndi] = y
+    x = run_flow(nd, yn)[ndi]
+    ref = np.linalg.solve(E, y)
+    assert np.abs(x - ref).max() <= 1e-12 * np.abs(ref).max()
