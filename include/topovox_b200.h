@@ -63,6 +63,17 @@ int tvb_matvec(int nx, int ny, int nz, const double* h_mh45, const double* d_u, 
  * out7 = {threads, wx, wy, tiles_x, tiles_y, persistent CTAs, 0} */
 int tvb_matvec_plan(int nx, int ny, int nz, int* h_out7);
 
+/* a3 with HOST buffers (the reference's StiffnessOperator.apply takes and
+ * returns numpy arrays, topovox/fea.py:49-65): out = K u with h_u / h_out in
+ * host memory (pinned for overlap), pipelined over `slabs` z-slabs of node
+ * planes (<= 0: default 6) so the host->device copy, the multiply and the
+ * device->host copy of successive slabs overlap. flags: MASK_IN / MASK_OUT
+ * (no ACCUMULATE). d_ws >= tvb_matvec_host_ws_bytes(). Synchronous. */
+size_t tvb_matvec_host_ws_bytes(int nx, int ny, int nz);
+int tvb_matvec_host(int nx, int ny, int nz, const double* h_mh45, const double* h_u, double* h_out,
+                    const double* d_occ, const uint8_t* d_nflags, int flags, int slabs, void* d_ws, size_t ws_bytes,
+                    void* stream);
+
 /* diagnostics: sustained fp64 FMA throughput of this GPU measured live
  * (independent DFMA chains on every SM), in TFLOP/s (2 flops per FMA);
  * the denominator of the north-star fp64 roofline. Synchronous. */

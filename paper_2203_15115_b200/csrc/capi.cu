@@ -1,4 +1,5 @@
 // extern "C" boundary of libtopovox_b200.so (declarations: include/topovox_b200.h).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -247,6 +248,98 @@ int tvb_matvec(int nx, int ny, int nz, const double* h_mh45, const double* d_u, 
   if (st || !d_dot) return st;
   k_sum_partials<<<1, 256, 0, s>>>((const double*)d_ws, pl.nblocks(), d_dot);
   return check(cudaGetLastError());
+}
+
+size_t tvb_matvec_host_ws_bytes(int nx, int ny, int nz) {
+  if (bad_dims(nx, ny, nz)) return 0;
+  return 2 * sizeof(double) * 3 * (size_t)make_grid(nx, ny, nz).nn + 256;
+}
+
+// Host-buffer K.u, pipelined over z-slabs of node planes: slab k's input
+// planes go host->device on one copy stream while slab k-1 is multiplied and
+// slab k-2's output planes go device->host on a second copy stream (the two
+// copy engines run concurrently), so a step costs about max(H2D, D2H) instead
+// of H2D + K.u + D2H. Node planes are contiguous in the reference numbering
+// (z slowest), so every slab copy is one contiguous range. Synchronous.
+int tvb_matvec_host(int nx, int ny, int nz, const double* h_mh45, const double* h_u, double* h_out,
+                    const double* d_occ, const uint8_t* d_nflags, int flags, int slabs, void* d_ws, size_t ws_bytes,
+                    void* stream) {
+  if (bad_dims(nx, ny, nz) || !h_mh45 || !h_u || !h_out || !d_occ || !d_ws) return kStatusBadArg;
+  if ((flags & (TVB_MASK_IN | TVB_MASK_OUT)) && !d_nflags) return kStatusBadArg;
+  if (flags & TVB_ACCUMULATE) {
+    set_last_error("tvb_matvec_host: ACCUMULATE is not supported for host buffers");
+    return kStatusBadArg;
+  }
+  if (ws_bytes < tvb_matvec_host_ws_bytes(nx, ny, nz)) {
+    set_last_error("matvec workspace too small");
+    return kStatusWorkspace;
+  }
+  Modal M;
+  if (!modal_reduce(h_mh45, M)) return kStatusBadArg;
+  const Grid g = make_grid(nx, ny, nz);
+  const MatvecPlan pl = plan_matvec(g, num_sms());
+  const size_t pdoubles = 3 * (size_t)g.px * g.py;  // doubles per node plane
+  double* du = (double*)(((uintptr_t)d_ws + 255) & ~(uintptr_t)255);
+  double* dy = du + 3 * (size_t)g.nn;
+  cudaStream_t s = (cudaStream_t)stream;
+  // default 6 slabs: measured best at 128^3 (4-8 within noise; 1 slab = no overlap, 1.31x slower)
+  const int K = std::max(1, std::min(slabs > 0 ? slabs : 6, g.pz / 2));
+
+  struct Pipe {
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t start = nullptr, in[64], done[64], end = nullptr;
+  };
+  static thread_local Pipe P;
+  if (P.h2d == nullptr) {
+    cudaStreamCreateWithFlags(&P.h2d, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&P.d2h, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&P.start, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&P.end, cudaEventDisableTiming);
+    for (int k = 0; k < 64; ++k) {
+      cudaEventCreateWithFlags(&P.in[k], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&P.done[k], cudaEventDisableTiming);
+    }
+  }
+  const int KK = std::min(K, 64);
+  // the copy streams start after the work already queued on the caller's stream
+  cudaEventRecord(P.start, s);
+  cudaStreamWaitEvent(P.h2d, P.start, 0);
+  cudaStreamWaitEvent(P.d2h, P.start, 0);
+  int loaded = 0;  // input planes [0, loaded) issued
+  for (int k = 0; k < KK; ++k) {
+    const int z0 = (int)((long long)g.pz * k / KK), z1 = (int)((long long)g.pz * (k + 1) / KK);
+    const int need = std::min(g.pz, z1 + 1);  // output planes [z0, z1) read input planes up to z1
+    if (need > loaded) {
+      cudaMemcpyAsync(du + pdoubles * loaded, h_u + pdoubles * loaded, sizeof(double) * pdoubles * (need - loaded),
+                      cudaMemcpyHostToDevice, P.h2d);
+      if (flags & TVB_MASK_IN) {
+        const long long n0 = (long long)g.px * g.py * loaded, nn = (long long)g.px * g.py * (need - loaded);
+        k_masked_copy<<<(unsigned)((3 * nn + 255) / 256), 256, 0, P.h2d>>>(nn, du + 3 * n0, d_nflags + n0,
+                                                                             du + 3 * n0);
+      }
+      loaded = need;
+    }
+    cudaEventRecord(P.in[k], P.h2d);
+    cudaStreamWaitEvent(s, P.in[k], 0);
+    MatvecParams mp{};
+    mp.g = g;
+    mp.u = du;
+    mp.y = dy;
+    mp.occ = d_occ;
+    mp.fixed = d_nflags;
+    mp.mask_out = (flags & TVB_MASK_OUT) ? 1 : 0;
+    mp.zlo = z0;
+    mp.zhi = z1;
+    const int st = check(launch_matvec(pl, mp, M, s));
+    if (st) return st;
+    cudaEventRecord(P.done[k], s);
+    cudaStreamWaitEvent(P.d2h, P.done[k], 0);
+    cudaMemcpyAsync(h_out + pdoubles * z0, dy + pdoubles * z0, sizeof(double) * pdoubles * (z1 - z0),
+                    cudaMemcpyDeviceToHost, P.d2h);
+  }
+  cudaEventRecord(P.end, P.d2h);
+  cudaStreamWaitEvent(s, P.end, 0);
+  return check(cudaStreamSynchronize(s));
 }
 
 double tvb_fp64_peak_tflops(void* stream) {

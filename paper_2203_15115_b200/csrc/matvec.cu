@@ -135,12 +135,13 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
   // Balanced persistent split: the work is tiles x pz node planes, flattened
   // tile-major; CTA b takes the contiguous range [w0, w1) and walks it as
   // (tile, plane range) pieces.
-  const long long W = (long long)P.ntiles * G.pz;
+  const int zlo = P.zlo, zhi = P.zhi < 0 ? G.pz : P.zhi, npl = zhi - zlo;  // output node planes
+  const long long W = (long long)P.ntiles * npl;
   const long long w0 = W * blockIdx.x / gridDim.x, w1 = W * (blockIdx.x + 1) / gridDim.x;
   for (long long w = w0; w < w1;) {
-    const int tile = (int)(w / G.pz);
-    const int kz0 = (int)(w % G.pz);
-    const int kz1 = (int)min((long long)G.pz, kz0 + (w1 - w));  // owned node planes [kz0, kz1)
+    const int tile = (int)(w / npl);
+    const int kz0 = zlo + (int)(w % npl);
+    const int kz1 = (int)min((long long)zhi, kz0 + (w1 - w));  // owned node planes [kz0, kz1)
     w += kz1 - kz0;
     const int x0 = (tile % P.ntx) * (wx - 1);
     const int y0 = (tile / P.ntx) * (wy - 1);

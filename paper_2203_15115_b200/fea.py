@@ -127,9 +127,42 @@ class StiffnessOperator:
 
     def apply(self, u, raw: bool = False):
         """K @ u. With raw=True the Dirichlet rows/columns are kept
-        (reference ``topovox/fea.py:49-65``)."""
-        u_d, np_in = to_device(u, self.n_dofs, "displacement vector")
-        return to_host_if(self.apply_device(u_d, raw=raw), np_in)
+        (reference ``topovox/fea.py:49-65``). Host input (numpy / CPU tensor)
+        returns host output through the pipelined host path (apply_host)."""
+        torch = _torch()
+        if isinstance(u, torch.Tensor) and u.is_cuda:
+            return self.apply_device(u, raw=raw)
+        return self.apply_host(u, raw=raw)
+
+    def apply_host(self, u, out=None, raw: bool = False, slabs: int = 0):
+        """K @ u for host vectors (numpy or CPU torch tensor; pinned memory
+        lets the copies overlap): z-slab pipeline of host->device copy,
+        multiply and device->host copy (``tvb_matvec_host``). Returns ``out``
+        (allocated like ``u`` when None)."""
+        torch = _torch()
+        tensor_in = isinstance(u, torch.Tensor)
+        if tensor_in:
+            if u.dtype != torch.float64 or u.numel() != self.n_dofs:
+                raise DimensionMismatch(f"displacement vector has {tuple(u.shape)}, expected ({self.n_dofs},)")
+            u_c = u.contiguous()
+            if out is None:
+                out = torch.empty(self.n_dofs, dtype=torch.float64, pin_memory=u_c.is_pinned())
+            pu, po = u_c.data_ptr(), out.data_ptr()
+        else:
+            u_c = np.ascontiguousarray(u, dtype=np.float64)
+            if u_c.shape != (self.n_dofs,):
+                raise DimensionMismatch(f"displacement vector has {u_c.shape}, expected ({self.n_dofs},)")
+            if out is None:
+                out = np.empty(self.n_dofs)
+            pu, po = u_c.ctypes.data, out.ctypes.data
+        need = lib().tvb_matvec_host_ws_bytes(*self._dims())
+        if getattr(self, "_host_ws", None) is None or self._host_ws.numel() < need:
+            self._host_ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+        flags = 0 if (raw or not self.dirichlet.size) else (_lib.MASK_IN | _lib.MASK_OUT)
+        check(lib().tvb_matvec_host(*self._dims(), self._mh.ctypes.data, pu, po, ptr(self.occ_d), ptr(self.nflags),
+                                    flags, int(slabs), ptr(self._host_ws), self._host_ws.numel(), stream_ptr()),
+              "matvec (host buffers)")
+        return out
 
     def apply_subset(self, u, elems):
         """K @ u using only the listed elements (reference ``fea.py:67-76``)."""
