@@ -1,4 +1,5 @@
-"""Summarise an ncu --set full report (first matching kernel) into JSON."""
+"""Summarise an ncu --set full report into JSON: `ncu_summarize.py REP KEY [ROW]`
+(ROW = index of the profiled launch in the report, default 0)."""
 import csv
 import io
 import json
@@ -6,9 +7,10 @@ import subprocess
 import sys
 
 rep, key = sys.argv[1], sys.argv[2]
+row = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
-hdr, units, vals = rows[0], rows[1], rows[2]
+hdr, units, vals = rows[0], rows[1], rows[2 + row]
 m = dict(zip(hdr, vals))
 u = dict(zip(hdr, units))
 SCALE = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
