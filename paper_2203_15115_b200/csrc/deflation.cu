@@ -8,6 +8,7 @@
 // block's closed node box followed by S^T; prolongation evaluates the rigid
 // motion t + omega x r of every block containing a node.
 #include <algorithm>
+#include <cstdlib>
 
 #include "deflation.cuh"
 #include "vec.cuh"

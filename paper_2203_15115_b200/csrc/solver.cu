@@ -247,9 +247,8 @@ int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
   auto one_iteration = [&]() -> cudaError_t {
     cudaError_t e = matvec(W.p, W.q, true, stop);
     if (e != cudaSuccess) return e;
-    e = launch_finalize_pq(W.partials + 2 * kMaxReduceCtas, plan.nblocks(), W.st, s);
-    if (e != cudaSuccess) return e;
-    e = launch_pcg_update(nd, P.x, W.r, W.z, W.p, W.q, W.inv_d, W.st, W.partials, s);
+    e = launch_pcg_update(nd, P.x, W.r, W.z, W.p, W.q, W.inv_d, W.st, W.partials, W.partials + 2 * kMaxReduceCtas,
+                          plan.nblocks(), s);
     if (e != cudaSuccess) return e;
     if (defl) {
       e = matvec(W.z, W.t, false, stop);
@@ -271,9 +270,9 @@ int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
     for (; nit < 20; ++nit) {
       cudaEventRecord(ev[0], s);
       matvec(W.p, W.q, true, stop);
-      launch_finalize_pq(W.partials + 2 * kMaxReduceCtas, plan.nblocks(), W.st, s);
       cudaEventRecord(ev[1], s);
-      launch_pcg_update(nd, P.x, W.r, W.z, W.p, W.q, W.inv_d, W.st, W.partials, s);
+      launch_pcg_update(nd, P.x, W.r, W.z, W.p, W.q, W.inv_d, W.st, W.partials, W.partials + 2 * kMaxReduceCtas,
+                        plan.nblocks(), s);
       cudaEventRecord(ev[2], s);
       if (defl) {
         matvec(W.z, W.t, false, stop);

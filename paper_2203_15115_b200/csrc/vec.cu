@@ -136,10 +136,26 @@ __global__ void __launch_bounds__(256) k_pcg_update_v2(long long n, double* __re
                                                        double* __restrict__ z, const double* __restrict__ p,
                                                        const double* __restrict__ q,
                                                        const double* __restrict__ inv_d, SolverState* st,
-                                                       double* partials) {
+                                                       double* partials, const double* pq_parts, int n_parts) {
   __shared__ double red[32];
+  __shared__ double s_pq;
   if (st->done) return;
-  const double alpha = st->rz / st->pq;
+  // p.q from the matvec's per-CTA partials, summed by every CTA in the same
+  // fixed order (replaces a separate finaliser launch)
+  if (pq_parts != nullptr) {
+    if (threadIdx.x < 32) {
+      double s = 0.0;
+      for (int i = threadIdx.x; i < n_parts; i += 32) s += __ldcg(pq_parts + i);
+      s = warp_sum(s);
+      if (threadIdx.x == 0) s_pq = s;
+    }
+    __syncthreads();
+  } else if (threadIdx.x == 0) {
+    s_pq = st->pq;
+  }
+  __syncthreads();
+  const double pq = s_pq;
+  const double alpha = st->rz / pq;
   const long long n2 = n >> 1;
   const long long per = (n2 + gridDim.x - 1) / gridDim.x;
   const long long lo = blockIdx.x * per, hi = min(n2, lo + per);
@@ -193,6 +209,7 @@ __global__ void __launch_bounds__(256) k_pcg_update_v2(long long n, double* __re
     partials[2 * blockIdx.x + 1] = rz;
   }
   finalize_last<2>(partials, gridDim.x, &st->counter, red, [&](double* t) {
+    st->pq = pq;
     st->alpha = alpha;
     st->iter += 1;
     st->rr = t[0];
@@ -307,12 +324,17 @@ cudaError_t launch_dot(const double* a, const double* b, const double* w, long l
 }
 
 cudaError_t launch_pcg_update(long long n, double* x, double* r, double* z, const double* p, const double* q,
-                              const double* inv_d, SolverState* st, double* partials, cudaStream_t s) {
+                              const double* inv_d, SolverState* st, double* partials, const double* pq_parts,
+                              int n_parts, cudaStream_t s) {
   const bool vec16 = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(r) |
                        reinterpret_cast<uintptr_t>(z) | reinterpret_cast<uintptr_t>(p) |
                        reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(inv_d)) & 15) == 0;
-  if (vec16) k_pcg_update_v2<<<reduce_grid(n), 256, 0, s>>>(n, x, r, z, p, q, inv_d, st, partials);
-  else k_pcg_update<<<reduce_grid(n), 256, 0, s>>>(n, x, r, z, p, q, inv_d, st, partials);
+  if (vec16) {
+    k_pcg_update_v2<<<reduce_grid(n), 256, 0, s>>>(n, x, r, z, p, q, inv_d, st, partials, pq_parts, n_parts);
+  } else {
+    if (pq_parts != nullptr) k_finalize_pq<<<1, 256, 0, s>>>(pq_parts, n_parts, st);
+    k_pcg_update<<<reduce_grid(n), 256, 0, s>>>(n, x, r, z, p, q, inv_d, st, partials);
+  }
   return cudaGetLastError();
 }
 

@@ -29,8 +29,11 @@ cudaError_t launch_inv_diag(const Grid& G, const double* occ, const uint8_t* nfl
                             double* inv_d, double* diag_out, int* zero_free, cudaStream_t s, int accumulate = 0);
 cudaError_t launch_dot(const double* a, const double* b, const double* w, long long n, double* ws,
                        unsigned int* counter, double* out, cudaStream_t s);
+// pq_parts (optional): the matvec's per-CTA p.q partials (n_parts), summed in
+// the update kernel itself; nullptr = st->pq already final
 cudaError_t launch_pcg_update(long long n, double* x, double* r, double* z, const double* p, const double* q,
-                              const double* inv_d, SolverState* st, double* partials, cudaStream_t s);
+                              const double* inv_d, SolverState* st, double* partials, const double* pq_parts,
+                              int n_parts, cudaStream_t s);
 cudaError_t launch_pcg_pupdate(long long n, double* p, const double* z, const SolverState* st, cudaStream_t s);
 cudaError_t launch_finalize_pq(const double* partials, int nparts, SolverState* st, cudaStream_t s);
 cudaError_t launch_pcg_init(long long n, const double* f, double* r, double* z, const double* inv_d,
