@@ -311,8 +311,16 @@ def dpcg_roofline(d, defl, us_per_iter, p64, hbm):
     stages = {"matvec_x2": 2 * t_mv, "update": 8 * vec / (hbm * 1e9), "restrict": 2 * vec / (hbm * 1e9),
               "coarse": coarse_bytes / (hbm * 1e9), "prolong": 3 * vec / (hbm * 1e9)}
     t_star = sum(stages.values())
+    # SURVEY §8(d) definition (reference algorithm): K p + (KW)^T z as W^T(K z)
+    # (bytes 8(N_d + N_e)), 11 vector passes (88 B/DOF), banded coarse sweeps
+    # 16 n_c w with w = 6 (m1 m2 + m1 + 1), m sorted ascending.
+    m = sorted(defl.grid)
+    w = 6 * (m[0] * m[1] + m[0] + 1)
+    t_r = max(1152.0 * d.n_elems / (p64 * 1e12), 8.0 * (d.n_dofs + d.n_elems) / (hbm * 1e9))
+    t_survey = t_mv + t_r + 88.0 * d.n_dofs / (hbm * 1e9) + 16.0 * 6 * defl.n_blocks * w / (hbm * 1e9)
     return {"t_star_us": t_star * 1e6, "frac": t_star * 1e6 / us_per_iter,
             "stages_us": {k: round(v * 1e6, 2) for k, v in stages.items()},
+            "survey_def": {"t_star_us": t_survey * 1e6, "frac": t_survey * 1e6 / us_per_iter},
             "p64_tflops": p64, "hbm_gbs": hbm}
 
 
