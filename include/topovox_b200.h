@@ -145,8 +145,8 @@ typedef struct tvb_coarse_nd {
   const int* d_udof;
   double* d_fS;
   double* d_cU;
-  const int* d_fwd_items;   /* (node, row0, row1) */
-  const int* d_bwd_items;
+  const long long* d_fwd_items;  /* [n][10]: the node's meta row (7), 0, row0, row1 */
+  const long long* d_bwd_items;
   const long long* h_fwd_ptr;  /* n_levels+1 work-item group offsets */
   const long long* h_bwd_ptr;
   const int* h_fwd_wpr;     /* warps per row per group (1,2,4,8) */

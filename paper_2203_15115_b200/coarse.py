@@ -51,10 +51,13 @@ SPLIT_FRONT = int(os.environ.get("TVB_ND_SPLIT_FRONT", "2048"))
 #: largest top set inverted densely (DOFs); the top tree levels it replaces
 #: would otherwise cost two latency-bound launches each
 TOP_MAX = int(os.environ.get("TVB_ND_TOP_MAX", "4608"))
-#: 1 = one persistent dataflow launch per solve, 0 = one launch per tree level
-#: (default: measured 10-20 % faster at C3/C4a/C5 -- inside a CUDA graph the
-#: per-level launch gap is smaller than the dataflow items' counter traffic)
-FLOW = os.environ.get("TVB_ND_FLOW", "0") != "0"
+#: schedule of the per-iteration solve: "1" = one persistent dataflow launch,
+#: "0" = one launch per tree level, unset = by size: the level schedule is
+#: 15-20 % faster for 12k coarse DOFs (C3/C4: inside a CUDA graph the per-level
+#: launch gap is smaller than the dataflow items' counter traffic), the
+#: dataflow one ~5 % faster from ~50k (C5: many items per level overlap)
+FLOW = os.environ.get("TVB_ND_FLOW")
+FLOW_MIN_DOFS = 48000
 #: target warps per solve launch (148 SMs x 16)
 WARPS_IN_FLIGHT = int(os.environ.get("TVB_ND_WARPS", "2368"))
 #: dynamic shared memory per CTA (B200: 227 KB opt-in)
@@ -400,6 +403,17 @@ class NDCoarseSolver:
         self.top_wpr = self._mode(self.n_top, np.array([self.n_top]))
         self.fwd_items = torch.from_numpy(np.array(fwd or [(0, 0, 0)], dtype=np.int32).reshape(-1, 3)).to(dev)
         self.bwd_items = torch.from_numpy(np.array(bwd or [(0, 0, 0)], dtype=np.int32).reshape(-1, 3)).to(dev)
+        # device item records of the level schedule: the node's meta row, 0, row0, row1
+        # (one round trip per CTA instead of item -> node -> meta)
+        def records(lst):
+            a = np.array(lst or [(0, 0, 0)], dtype=np.int64).reshape(-1, 3)
+            rec = np.zeros((a.shape[0], 10), dtype=np.int64)
+            rec[:, :8] = meta[a[:, 0]]
+            rec[:, 8:] = a[:, 1:]
+            return torch.from_numpy(rec).to(dev)
+
+        self.fwd_rec = records(fwd)
+        self.bwd_rec = records(bwd)
         self.fwd_ptr = np.array(fptr, dtype=np.int64)
         self.bwd_ptr = np.array(bptr, dtype=np.int64)
         self.fwd_wpr = np.array(fw or [1], dtype=np.int32)
@@ -506,7 +520,7 @@ class NDCoarseSolver:
         d.d_meta, d.d_gmap = ptr(self.meta), ptr(self.gmap)
         d.d_G, d.d_B = ptr(self.G), ptr(self.B)
         d.d_udof, d.d_fS, d.d_cU = ptr(self.udof), ptr(self.fS), ptr(self.cU)
-        d.d_fwd_items, d.d_bwd_items = ptr(self.fwd_items), ptr(self.bwd_items)
+        d.d_fwd_items, d.d_bwd_items = ptr(self.fwd_rec), ptr(self.bwd_rec)
         d.h_fwd_ptr = self._host_array(ctypes.c_longlong, self.fwd_ptr.tolist())
         d.h_bwd_ptr = self._host_array(ctypes.c_longlong, self.bwd_ptr.tolist())
         d.h_fwd_wpr = self._host_array(ctypes.c_int, self.fwd_wpr.tolist())
@@ -518,7 +532,8 @@ class NDCoarseSolver:
         d.d_ZT, d.d_fT = ptr(self.ZT), ptr(self.fT)
         d.d_tptr, d.d_tidx = ptr(self.tptr), ptr(self.tidx)
         d.d_perm = ptr(self.perm)
-        if FLOW:
+        flow = FLOW != "0" if FLOW is not None else 6 * self.nb >= FLOW_MIN_DOFS
+        if flow:
             d.d_items, d.n_items, d.d_rel = ptr(self.items), self.n_items, ptr(self.rel)
             d.d_cnt, d.d_ctl = ptr(self.cnt), ptr(self.ctl)
         d.d_factor, d.factor_bytes = ptr(self.factor), self.bytes

@@ -199,11 +199,46 @@ __device__ __forceinline__ void fill_batched(double* dst, int n, F f) {
 // Forward rows: c_U[j] = f_U[j] - G[j,:] f_S. assembled: f_S / f_U were written
 // by the node's assembly item; else gathered here (the node's first item
 // also stores f_S for the backward pass).
-__device__ __forceinline__ void item_fwd(const CoarseNDDev& D, bool assembled, int wpr, int node, int r0, int r1,
-                                         const double* y, double* fs, double* red) {
-  const long long* m = D.meta + 8 * node;
-  const int s = (int)m[0];
-  const long long g_off = m[2], sd_off = m[4], ud_off = m[5], gm = m[6];
+// A bottom node's layout (meta row: s, u, g_off, b_off, sd_off, ud_off, gm_off).
+struct NodeInfo {
+  int s, u;
+  long long g_off, b_off, sd_off, ud_off, gm;
+};
+
+__device__ __forceinline__ NodeInfo node_info(const long long* __restrict__ m) {
+  NodeInfo n;
+  n.s = (int)__ldg(m);
+  n.u = (int)__ldg(m + 1);
+  n.g_off = __ldg(m + 2);
+  n.b_off = __ldg(m + 3);
+  n.sd_off = __ldg(m + 4);
+  n.ud_off = __ldg(m + 5);
+  n.gm = __ldg(m + 6);
+  return n;
+}
+
+// per-launch item record (level schedule): the node's meta row + rows [r0, r1),
+// 10 x int64, read with independent 16-byte loads (one round trip)
+__device__ __forceinline__ NodeInfo item_record(const long long* __restrict__ rec, int& r0, int& r1) {
+  const longlong2* q = reinterpret_cast<const longlong2*>(rec);
+  const longlong2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2), d = __ldg(q + 3), e = __ldg(q + 4);
+  NodeInfo n;
+  n.s = (int)a.x;
+  n.u = (int)a.y;
+  n.g_off = b.x;
+  n.b_off = b.y;
+  n.sd_off = c.x;
+  n.ud_off = c.y;
+  n.gm = d.x;
+  r0 = (int)e.x;
+  r1 = (int)e.y;
+  return n;
+}
+
+__device__ __forceinline__ void item_fwd(const CoarseNDDev& D, bool assembled, int wpr, const NodeInfo& n, int r0,
+                                         int r1, const double* y, double* fs, double* red) {
+  const int s = n.s;
+  const long long g_off = n.g_off, sd_off = n.sd_off, ud_off = n.ud_off, gm = n.gm;
   if (assembled) {
     fill_batched(fs, s, [&](int i) { return __ldcg(D.fS + sd_off + i); });
   } else {
@@ -221,10 +256,9 @@ __device__ __forceinline__ void item_fwd(const CoarseNDDev& D, bool assembled, i
 }
 
 // Large fronts, assembly: f_S -> fS, f_U -> cU (whole node).
-__device__ __forceinline__ void item_asm(const CoarseNDDev& D, int node, const double* y) {
-  const long long* m = D.meta + 8 * node;
-  const int s = (int)m[0], u = (int)m[1];
-  const long long sd_off = m[4], ud_off = m[5], gm = m[6];
+__device__ __forceinline__ void item_asm(const CoarseNDDev& D, const NodeInfo& n, const double* y) {
+  const int s = n.s, u = n.u;
+  const long long sd_off = n.sd_off, ud_off = n.ud_off, gm = n.gm;
   batched(
       s + u, [&](int p) { return gather_front(D, gm, p, p < s ? y[sd_off + p] : 0.0); },
       [&](int p, double v) {
@@ -234,11 +268,10 @@ __device__ __forceinline__ void item_asm(const CoarseNDDev& D, int node, const d
 }
 
 // Backward rows: x_S[j] = [Z | -G^T][j,:] . [f_S ; x_U].
-__device__ __forceinline__ void item_bwd(const CoarseNDDev& D, int wpr, int node, int r0, int r1, double* x,
+__device__ __forceinline__ void item_bwd(const CoarseNDDev& D, int wpr, const NodeInfo& n, int r0, int r1, double* x,
                                          double* v, double* red) {
-  const long long* m = D.meta + 8 * node;
-  const int s = (int)m[0], u = (int)m[1];
-  const long long b_off = m[3], sd_off = m[4], ud_off = m[5];
+  const int s = n.s, u = n.u;
+  const long long b_off = n.b_off, sd_off = n.sd_off, ud_off = n.ud_off;
   fill_batched(v, s + u, [&](int i) {
     return i < s ? __ldcg(D.fS + sd_off + i) : __ldcg(x + __ldg(D.udof + ud_off + i - s));
   });
@@ -310,12 +343,12 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_flow(CoarseNDDev D, c
     }
     __syncthreads();
     switch (type) {
-      case kFwd: item_fwd(D, false, wpr, node, r0, r1, y, sm, red); break;
-      case kAsm: item_asm(D, node, y); break;
-      case kRows: item_fwd(D, true, wpr, node, r0, r1, y, sm, red); break;
+      case kFwd: item_fwd(D, false, wpr, node_info(D.meta + 8 * node), r0, r1, y, sm, red); break;
+      case kAsm: item_asm(D, node_info(D.meta + 8 * node), y); break;
+      case kRows: item_fwd(D, true, wpr, node_info(D.meta + 8 * node), r0, r1, y, sm, red); break;
       case kTopGather: item_top_gather(D, r0, r1, y); break;
       case kTopRows: item_top_rows(D, wpr, r0, r1, x, sm, red); break;
-      default: item_bwd(D, wpr, node, r0, r1, x, sm, red); break;
+      default: item_bwd(D, wpr, node_info(D.meta + 8 * node), r0, r1, x, sm, red); break;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -341,27 +374,30 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_flow(CoarseNDDev D, c
 
 // ---- per-level schedule (fallback) -----------------------------------------
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_fwd(CoarseNDDev D, int wpr, int assembled,
-                                                               const int* items, const double* y, const int* stop) {
+                                                               const long long* recs, const double* y,
+                                                               const int* stop) {
   extern __shared__ double sm[];
   __shared__ double red[4 * kCoarseWarps];
   if (stop != nullptr && *stop) return;
-  const int* it = items + 3 * blockIdx.x;
-  item_fwd(D, assembled != 0, wpr, it[0], it[1], it[2], y, sm, red);
+  int r0, r1;
+  const NodeInfo n = item_record(recs + 10LL * blockIdx.x, r0, r1);
+  item_fwd(D, assembled != 0, wpr, n, r0, r1, y, sm, red);
 }
 
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_asm(CoarseNDDev D, const int* nodes, const double* y,
                                                                const int* stop) {
   if (stop != nullptr && *stop) return;
-  item_asm(D, nodes[blockIdx.x], y);
+  item_asm(D, node_info(D.meta + 8 * nodes[blockIdx.x]), y);
 }
 
-__global__ void __launch_bounds__(kCoarseThreads) k_coarse_bwd(CoarseNDDev D, int wpr, const int* items, double* x,
-                                                               const int* stop) {
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_bwd(CoarseNDDev D, int wpr, const long long* recs,
+                                                               double* x, const int* stop) {
   extern __shared__ double sm[];
   __shared__ double red[4 * kCoarseWarps];
   if (stop != nullptr && *stop) return;
-  const int* it = items + 3 * blockIdx.x;
-  item_bwd(D, wpr, it[0], it[1], it[2], x, sm, red);
+  int r0, r1;
+  const NodeInfo n = item_record(recs + 10LL * blockIdx.x, r0, r1);
+  item_bwd(D, wpr, n, r0, r1, x, sm, red);
 }
 
 __global__ void k_coarse_top_gather(CoarseNDDev D, const double* y, const int* stop) {
@@ -418,7 +454,7 @@ cudaError_t launch_coarse_nd(const CoarseNDDev& D, const double* y, double* x, c
       const long long na = D.asm_ptr[h], nb = D.asm_ptr[h + 1];
       k_coarse_asm<<<(unsigned)(nb - na), kCoarseThreads, 0, s>>>(D, D.asm_nodes + na, y, stop);
     }
-    k_coarse_fwd<<<(unsigned)(b - a), kCoarseThreads, smem_fwd, s>>>(D, D.fwd_wpr[h], split, D.fwd_items + 3 * a, y,
+    k_coarse_fwd<<<(unsigned)(b - a), kCoarseThreads, smem_fwd, s>>>(D, D.fwd_wpr[h], split, D.fwd_items + 10 * a, y,
                                                                       stop);
   }
   if (D.n_top > 0) {
@@ -429,7 +465,7 @@ cudaError_t launch_coarse_nd(const CoarseNDDev& D, const double* y, double* x, c
   for (int h = 0; h < D.n_levels; ++h) {  // bwd groups: top-most bottom level first
     const long long a = D.bwd_ptr[h], b = D.bwd_ptr[h + 1];
     if (b > a)
-      k_coarse_bwd<<<(unsigned)(b - a), kCoarseThreads, smem_bwd, s>>>(D, D.bwd_wpr[h], D.bwd_items + 3 * a, x, stop);
+      k_coarse_bwd<<<(unsigned)(b - a), kCoarseThreads, smem_bwd, s>>>(D, D.bwd_wpr[h], D.bwd_items + 10 * a, x, stop);
   }
   return cudaGetLastError();
 }

@@ -15,8 +15,8 @@ struct CoarseNDDev {
   const int* udof;            // per node: update-set coarse DOFs (ND numbering)
   double* fS;                 // ND-dof indexed scratch: assembled separator rhs
   double* cU;                 // per node scratch: update vector passed to the parent
-  const int* fwd_items;       // [n][3] (node, row0, row1), grouped by height (leaves first)
-  const int* bwd_items;       // [n][3], grouped by height (top bottom level first)
+  const long long* fwd_items; // [n][10] node meta row (7) + 0 + row0, row1; grouped by height (leaves first)
+  const long long* bwd_items; // [n][10], grouped by height (top bottom level first)
   const long long* fwd_ptr;   // host: n_levels+1 group offsets
   const long long* bwd_ptr;   // host
   const int* fwd_wpr;         // host, per group: warps per matrix row (1, 2, 4, 8)

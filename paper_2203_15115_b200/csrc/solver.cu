@@ -244,17 +244,29 @@ int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
 
   // --- iteration graph -----------------------------------------------------
   const int* stop = &W.st->done;
+  // TVB_SOLVE_SKIP (timing experiments only -- the iterates are then wrong):
+  // bitmask of iteration stages left out of the graph, 1 A p, 2 update, 4 A z,
+  // 8 restriction, 16 coarse solve, 32 nu + prolongation; the in-graph cost of
+  // a stage is the per-iteration time difference.
+  const int skip = getenv("TVB_SOLVE_SKIP") ? atoi(getenv("TVB_SOLVE_SKIP")) : 0;
   auto one_iteration = [&]() -> cudaError_t {
-    cudaError_t e = matvec(W.p, W.q, true, stop);
-    if (e != cudaSuccess) return e;
-    e = launch_pcg_update(nd, P.x, W.r, W.z, W.p, W.q, W.inv_d, W.st, W.partials, W.partials + 2 * kMaxReduceCtas,
-                          plan.nblocks(), s);
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
+    if (!(skip & 1) && (e = matvec(W.p, W.q, true, stop)) != cudaSuccess) return e;
+    if (!(skip & 2) &&
+        (e = launch_pcg_update(nd, P.x, W.r, W.z, W.p, W.q, W.inv_d, W.st, W.partials,
+                               W.partials + 2 * kMaxReduceCtas, plan.nblocks(), s)) != cudaSuccess)
+      return e;
     if (defl) {
-      e = matvec(W.z, W.t, false, stop);
-      if (e != cudaSuccess) return e;
-      e = coarse_project(W.t, stop, W.q);
-      if (e != cudaSuccess) return e;
+      if (!(skip & 4) && (e = matvec(W.z, W.t, false, stop)) != cudaSuccess) return e;
+      if (!(skip & 8) && (e = launch_restrict(A, P.nflags, D, W.t, W.yc, s, stop, W.q, W.st)) != cudaSuccess)
+        return e;
+      if (!(skip & 16)) {
+        e = P.coarse_kind == 1 ? launch_coarse_nd(P.nd, W.yc, W.mu, stop, s)
+                               : launch_dense_gemv(6 * A.nb, P.coarse, W.yc, W.mu, stop, s);
+        if (e != cudaSuccess) return e;
+      }
+      if (skip & 32) return cudaSuccess;
+      if ((e = launch_block_nu(A, D, W.mu, W.nu, s, stop)) != cudaSuccess) return e;
       return launch_prolong(A, P.nflags, D, W.nu, W.p, W.z, W.st, 1, s);
     }
     return launch_pcg_pupdate(nd, W.p, W.z, W.st, s);

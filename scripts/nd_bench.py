@@ -27,7 +27,7 @@ for name in sys.argv[1:] or ["C3", "C4a"]:
     Es = defl.Es
     row = {}
     for flow, tm in variants:
-        C.FLOW = bool(flow)
+        C.FLOW = "1" if flow else "0"
         nd = C.NDCoarseSolver(defl.grid, Es, top_max=tm)
         y = torch.randn(6 * nd.nb, dtype=torch.float64, device="cuda")
         x = torch.empty_like(y)

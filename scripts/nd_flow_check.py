@@ -14,7 +14,7 @@ import paper_2203_15115_b200.coarse as C  # noqa: E402
 
 cases = [((4, 3, 3), 27, 4608), ((5, 5, 10), 27, 0), ((9, 8, 7), 8, 60), ((9, 8, 7), 8, 4608), ((12, 10, 9), 27, 600)]
 for flow in (0, 1):
-    C.FLOW = bool(flow)
+    C.FLOW = "1" if flow else "0"
     for grid, leaf, tm in cases:
         Es = random_block_stencil(*grid, seed=1)
         E = dense_of(Es, *grid)
