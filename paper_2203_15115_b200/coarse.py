@@ -51,6 +51,10 @@ SPLIT_FRONT = int(os.environ.get("TVB_ND_SPLIT_FRONT", "2048"))
 #: largest top set inverted densely (DOFs); the top tree levels it replaces
 #: would otherwise cost two latency-bound launches each
 TOP_MAX = int(os.environ.get("TVB_ND_TOP_MAX", "4608"))
+#: largest leaf box of the dissection (blocks); default by size: 125 for
+#: coarse systems up to FLOW_MIN_DOFS (fewer, fatter tree levels: C4 coarse
+#: solve 86 -> 66 us in the iteration), 64 above (C5 / C2(b) are bandwidth-bound)
+LEAF_MAX = int(os.environ["TVB_ND_LEAF"]) if os.environ.get("TVB_ND_LEAF") else None
 #: schedule of the per-iteration solve: "1" = one persistent dataflow launch,
 #: "0" = one launch per tree level, unset = by size: the level schedule is
 #: 15-20 % faster for 12k coarse DOFs (C3/C4: inside a CUDA graph the per-level
@@ -139,13 +143,15 @@ class NDCoarseSolver:
     hold the device data of the per-iteration solve (``tvb_coarse_nd_solve``).
     Solve vectors are in ND order: natural block B sits at ND block ``perm[B]``."""
 
-    def __init__(self, grid: tuple[int, int, int], Es, leaf_max: int = 27, top_max: int | None = None,
+    def __init__(self, grid: tuple[int, int, int], Es, leaf_max: int | None = None, top_max: int | None = None,
                  make_desc: bool = True):
         import torch
 
         mx, my, mz = grid
         self.grid = grid
         self.nb = nb = mx * my * mz
+        if leaf_max is None:
+            leaf_max = LEAF_MAX if LEAF_MAX is not None else (125 if 6 * nb <= FLOW_MIN_DOFS else 64)
         nodes = nested_dissection(mx, my, mz, leaf_max)
         self.nodes = nodes
         H = max(n.height for n in nodes)
