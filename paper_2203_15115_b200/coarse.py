@@ -36,6 +36,7 @@ device (cuSOLVER/cuBLAS); it runs once per topology, not per iteration.
 from __future__ import annotations
 
 import ctypes
+import functools
 import logging
 import os
 from dataclasses import dataclass, field
@@ -68,6 +69,8 @@ WARPS_IN_FLIGHT = int(os.environ.get("TVB_ND_WARPS", "2368"))
 SMEM_MAX = 227 * 1024
 #: resident 256-thread CTAs on the GPU (148 SMs x 8): one wave of solve items
 CTA_SLOTS = int(os.environ.get("TVB_ND_SLOTS", "1184"))
+#: index plans of the numeric factorisation, keyed by (block grid, leaf, top, device)
+_PLAN_CACHE: dict = {}
 
 
 def mode_step(mode: int) -> int:
@@ -85,6 +88,7 @@ class NDNode:
     parent: int = -1
 
 
+@functools.lru_cache(maxsize=4)
 def nested_dissection(mx: int, my: int, mz: int, leaf_max: int = 27) -> list[NDNode]:
     """Geometric ND of the mx x my x mz block grid; nodes in postorder."""
     nodes: list[NDNode] = []
@@ -156,6 +160,7 @@ class NDCoarseSolver:
         self.nodes = nodes
         H = max(n.height for n in nodes)
         top_max = TOP_MAX if top_max is None else top_max
+        self.leaf_max, self.top_max = leaf_max, top_max
         seps_by_h = np.zeros(H + 2, dtype=np.int64)
         for n in nodes:
             seps_by_h[n.height] += 6 * n.sep.size
@@ -208,94 +213,122 @@ class NDCoarseSolver:
             out[3].append(np.full(int(keep.sum()), d))
         return [np.concatenate(o) for o in out]
 
-    def _scatter_blocks(self, torch, F, E6, rows, cols, srcB, srcD, mirror_from):
-        dev = F.device
-        blk = E6[torch.from_numpy(srcB).to(dev), torch.from_numpy(srcD).to(dev)]
-        ar = torch.arange(6, device=dev)
-        r6 = torch.from_numpy(6 * rows).to(dev)[:, None, None] + ar[None, :, None]
-        c6 = torch.from_numpy(6 * cols).to(dev)[:, None, None] + ar[None, None, :]
-        F[r6.expand(-1, 6, 6), c6.expand(-1, 6, 6)] = blk
+    def _flat_scatter(self, rows, cols, srcB, srcD, nf, mirror_from):
+        """Flat indices for F.view(-1)[fidx] = Es.view(-1)[eidx]: the 6x6 blocks
+        E[srcB, srcD] at block position (rows, cols) of an nf x nf front, plus
+        their transposes at (cols, rows) for cols >= mirror_from (block units)."""
+        i = np.arange(6)[None, :, None]
+        j = np.arange(6)[None, None, :]
+        r6, c6 = 6 * rows[:, None, None], 6 * cols[:, None, None]
+        e = ((srcB[:, None, None] * 27 + srcD[:, None, None]) * 6 + i) * 6 + j
+        f = (r6 + i) * nf + (c6 + j)
+        fl, el = [f.ravel()], [e.ravel()]
         if mirror_from is not None:
             m = cols >= mirror_from
             if m.any():
-                mt = torch.from_numpy(m).to(dev)
-                F[c6[mt].expand(-1, 6, 6).transpose(1, 2), r6[mt].expand(-1, 6, 6).transpose(1, 2)] = \
-                    blk[mt].transpose(1, 2)
+                fl.append(((c6[m] + j) * nf + (r6[m] + i)).ravel())
+                el.append(e[m].ravel())
+        return np.concatenate(fl), np.concatenate(el)
 
-    def _factor(self, torch, Es, nodes, bottom, top, bidx, perm):
-        dev = Es.device
+    def _plan(self, torch, dev, nodes, bottom, top, perm):
+        """Index plan of the numeric factorisation (depends on the block grid
+        only, so it is cached across topologies): per bottom node the flat
+        scatter of its original E entries into the front, the extend-add
+        positions of its children's updates, and the same for the dense top."""
         nb = self.nb
-        E6 = Es.view(nb, 27, 6, 6)
-        upd = {}
+        P = {"nodes": [], "top": None}
         ud_off = {}
         ud_cursor = 0
-        G_list, B_list = [], []
-        s_list, u_list, sd_list, udof_list, gmaps = [], [], [], [], []
         blk_cursor = 0
+        s_list, u_list, sd_list, udof_list, gmaps = [], [], [], [], []
         for ni in bottom:
             n = nodes[ni]
             ns, nu = n.sep.size, n.upd.size
             front = np.concatenate([n.sep, n.upd])
+            nf = 6 * front.size
             pos = -np.ones(nb, dtype=np.int64)
             pos[front] = np.arange(front.size)
-            F = torch.zeros((6 * front.size, 6 * front.size), dtype=torch.float64, device=dev)
             rows, cols, srcB, srcD = self._stencil_entries(n.sep, pos)
-            self._scatter_blocks(torch, F, E6, rows, cols, srcB, srcD, mirror_from=ns)
-            # gather map: front position -> (child 0, child 1) update-vector index
-            gm = -np.ones((6 * front.size, 2), dtype=np.int64)
+            fidx, eidx = self._flat_scatter(rows, cols, srcB, srcD, nf, ns)
+            gm = -np.ones((nf, 2), dtype=np.int64)
             assert len(n.children) <= 2
+            adds = []
             for k, c in enumerate(n.children):
                 m = _dofs(pos[nodes[c].upd])
-                Uc = upd.pop(c)
-                mt = torch.from_numpy(m).to(dev)
-                F[mt[:, None], mt[None, :]] += Uc
+                adds.append((c, torch.from_numpy((m[:, None] * nf + m[None, :]).ravel()).to(dev)))
                 gm[m, k] = ud_off[c] + np.arange(m.size)
             gmaps.append(gm.astype(np.int32).ravel())
-            S = 6 * ns
-            L, info = torch.linalg.cholesky_ex(0.5 * (F[:S, :S] + F[:S, :S].T))
-            if int(info.item()) != 0:
-                raise np.linalg.LinAlgError(f"coarse front {ni} not SPD")
-            Z = torch.cholesky_inverse(L)
-            G = F[S:, :S] @ Z
-            if nu:
-                upd[ni] = F[S:, S:] - G @ F[:S, S:]
-            G_list.append(G.contiguous())
-            B_list.append(torch.cat([Z, -G.T], dim=1).contiguous())   # x_S = [Z | -G^T] [f_S ; x_U]
-            s_list.append(S)
+            P["nodes"].append((ni, nf, 6 * ns, nu, torch.from_numpy(fidx).to(dev), torch.from_numpy(eidx).to(dev),
+                               adds))
+            s_list.append(6 * ns)
             u_list.append(6 * nu)
             sd_list.append(6 * blk_cursor)
             ud_off[ni] = ud_cursor
             ud_cursor += 6 * nu
             blk_cursor += ns
             udof_list.append(_dofs(perm[n.upd]).astype(np.int32))
-            del F
-        # ---- dense top: S_T = E_TT + updates of bottom nodes with a top parent
-        self.Ztop = None
         t_pos, t_idx = [], []
         if self.n_top:
             tblocks = np.concatenate([nodes[i].sep for i in top]).astype(np.int64)
             tpos = -np.ones(nb, dtype=np.int64)
             tpos[tblocks] = perm[tblocks] - (nb - tblocks.size)
-            ST = torch.zeros((self.n_top, self.n_top), dtype=torch.float64, device=dev)
             rows, cols, srcB, srcD = self._stencil_entries(tblocks, tpos)
-            rows = tpos[srcB]
-            self._scatter_blocks(torch, ST, E6, rows, cols, srcB, srcD, mirror_from=None)
+            fidx, eidx = self._flat_scatter(tpos[srcB], cols, srcB, srcD, self.n_top, None)
+            adds = []
             for ni in bottom:
                 if nodes[ni].parent >= 0 and nodes[nodes[ni].parent].height >= self.H0:
                     m = _dofs(tpos[nodes[ni].upd])
-                    mt = torch.from_numpy(m).to(dev)
-                    ST[mt[:, None], mt[None, :]] += upd.pop(ni)
+                    adds.append((ni, torch.from_numpy((m[:, None] * self.n_top + m[None, :]).ravel()).to(dev)))
                     t_pos.append(m)
                     t_idx.append(ud_off[ni] + np.arange(m.size))
+            P["top"] = (torch.from_numpy(fidx).to(dev), torch.from_numpy(eidx).to(dev), adds)
+        P["pack"] = (np.array(s_list, np.int64), np.array(u_list, np.int64), np.array(sd_list, np.int64),
+                     udof_list, gmaps, t_pos, t_idx, ud_cursor, [nodes[i].height for i in bottom])
+        return P
+
+    def _factor(self, torch, Es, nodes, bottom, top, bidx, perm):
+        dev = Es.device
+        key = (self.grid, self.leaf_max, self.top_max, str(dev))
+        plan = _PLAN_CACHE.get(key)
+        if plan is None:
+            plan = self._plan(torch, dev, nodes, bottom, top, perm)
+            _PLAN_CACHE.clear()  # keep one plan (one block grid per optimisation run)
+            _PLAN_CACHE[key] = plan
+        Ef = Es.reshape(-1)
+        upd = {}
+        G_list, B_list, infos = [], [], []
+        for ni, nf, S, nu, fidx, eidx, adds in plan["nodes"]:
+            F = torch.zeros(nf * nf, dtype=torch.float64, device=dev)
+            F[fidx] = Ef[eidx]
+            for c, cidx in adds:
+                F[cidx] += upd.pop(c).reshape(-1)
+            F = F.view(nf, nf)
+            L, info = torch.linalg.cholesky_ex(0.5 * (F[:S, :S] + F[:S, :S].T))
+            infos.append(info)
+            Z = torch.cholesky_inverse(L)
+            G = F[S:, :S] @ Z
+            if nu:
+                upd[ni] = F[S:, S:] - G @ F[:S, S:]
+            G_list.append(G.contiguous())
+            B_list.append(torch.cat([Z, -G.T], dim=1).contiguous())   # x_S = [Z | -G^T] [f_S ; x_U]
+            del F
+        # ---- dense top: S_T = E_TT + updates of bottom nodes with a top parent
+        self.Ztop = None
+        if self.n_top:
+            fidx, eidx, adds = plan["top"]
+            ST = torch.zeros(self.n_top * self.n_top, dtype=torch.float64, device=dev)
+            ST[fidx] = Ef[eidx]
+            for ni, cidx in adds:
+                ST[cidx] += upd.pop(ni).reshape(-1)
+            ST = ST.view(self.n_top, self.n_top)
             L, info = torch.linalg.cholesky_ex(0.5 * (ST + ST.T))
-            if int(info.item()) != 0:
-                raise np.linalg.LinAlgError("coarse top Schur complement not SPD")
+            infos.append(info)
             self.Ztop = torch.cholesky_inverse(L).contiguous()
             del ST, L
         assert not upd, "unconsumed update matrices"
-        self._pack(torch, dev, G_list, B_list, np.array(s_list, np.int64), np.array(u_list, np.int64),
-                   np.array(sd_list, np.int64), udof_list, gmaps, t_pos, t_idx, ud_cursor,
-                   [nodes[i].height for i in bottom])
+        if infos and bool(torch.stack(infos).ne(0).any()):  # one host sync for all fronts
+            raise np.linalg.LinAlgError("coarse front not SPD")
+        self._pack(torch, dev, G_list, B_list, *plan["pack"])
 
     @staticmethod
     def _wpr(rowlen: int, rows: int) -> int:
@@ -437,10 +470,14 @@ class NDCoarseSolver:
         self.asm_nodes = torch.from_numpy(np.array(asm or [0], dtype=np.int32)).to(dev)
         self.asm_ptr = np.array(aptr, dtype=np.int64)
         self.bytes = self.factor.numel() * 8
-        items, rel, ncnt = self._flow_items(s, u, heights)
-        self.n_items = len(items) // 12
-        self.items = torch.from_numpy(np.array(items, dtype=np.int32).reshape(-1, 12)).to(dev)
-        self.rel = torch.from_numpy(np.array(rel + [0], dtype=np.int32)).to(dev)
+        # dataflow items: structural, cached with the index plan
+        flow_key = ("flow", self.grid, self.leaf_max, self.top_max, str(dev))
+        if flow_key not in _PLAN_CACHE:
+            items, rel, ncnt = self._flow_items(s, u, heights)
+            _PLAN_CACHE[flow_key] = (len(items) // 12,
+                                     torch.from_numpy(np.array(items, dtype=np.int32).reshape(-1, 12)).to(dev),
+                                     torch.from_numpy(np.array(rel + [0], dtype=np.int32)).to(dev), ncnt)
+        self.n_items, self.items, self.rel, ncnt = _PLAN_CACHE[flow_key]
         self.cnt = torch.zeros(ncnt + 1, dtype=torch.int64, device=dev)
         self.ctl = torch.zeros(4, dtype=torch.int64, device=dev)
 
