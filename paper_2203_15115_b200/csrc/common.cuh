@@ -96,6 +96,10 @@ __device__ __forceinline__ double block_max(double v, double* scratch) {
 }
 
 // cp.async helpers (LDGSTS) ------------------------------------------------
+// smem given as a shared-window byte address (precomputed by the caller)
+__device__ __forceinline__ void cp_async8_s(unsigned smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem), "l"(gmem));
+}
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));

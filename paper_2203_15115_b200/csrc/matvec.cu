@@ -96,6 +96,7 @@ __device__ __forceinline__ void xy_inverse(double (&f)[12]) {
     }
 }
 
+constexpr int kStage = 4;   // max staged node-plane doubles per thread ((wy+1)*3(wx+1) <= kStage*NT)
 constexpr int kXcPad = 64;  // exchange rows past NT read (harmlessly) by edge threads
 constexpr int kAhead = 4;   // node planes in flight ahead of the compute (cp.async groups)
 constexpr int kRing = kAhead + 1;
@@ -125,6 +126,8 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
   double* Xc = Oc + kRing * OS;       // [2][NT + kXcPad][9] face exchange
   const int XS = 9 * (NT + kXcPad);
   double* red = Xc + 2 * XS;
+  unsigned* st_soff = reinterpret_cast<unsigned*>(red + NT / 32 + 1);  // [kStage][NT] staging lists
+  int* st_goff = reinterpret_cast<int*>(st_soff + kStage * NT);
 
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
@@ -167,31 +170,64 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
           for (int b = 0; b < kRing; ++b) Oc[b * OS + jy * wx + j] = 0.0;
     }
 
-    // stage node plane k and occupancy layer k (zero-filled outside the grid)
-    auto load_layer = [&](int k) {
-      double* dst = Up + ((k + kRing) % kRing) * PS;
-      const bool kin = k >= 0 && k < G.pz;
-      const double* src = P.u + plane_stride * (kin ? k : 0) + 3LL * (x0 - 1);
-      for (int jy = warp; jy < PH; jy += NT / 32) {
-        const int gy = y0 - 1 + jy;
-        if (gy < 0 || gy >= G.py) continue;
-        const double* srow = src + 3LL * G.px * gy;
-        double* drow = dst + jy * S;
-        for (int r = r_lo + lane; r < r_hi; r += 32) {
-          if (kin) cp_async8(drow + r, srow + r);
-          else drow[r] = 0.0;
+    // Per-thread staging assignment, fixed for all planes of the piece: the
+    // in-grid doubles of a staged node plane (rows x [r_lo, r_hi)) are dealt
+    // out round-robin, thread t taking elements t, t + NT, ...; each keeps the
+    // smem byte offset and the in-plane global offset of its <= kStage
+    // elements, so staging one plane is kStage predicated cp.async per thread
+    // (no per-plane row/column index arithmetic). Likewise one occupancy
+    // element per thread (wx * wy <= NT).
+    // (kept in shared memory, [kStage][NT] each: registers are the kernel's
+    // limiting resource)
+    int ncnt = 0;
+    {
+      const int rw = r_hi - r_lo;
+      const int jy_lo = max(0, 1 - y0), jy_hi = min(PH, G.py - y0 + 1);
+      const int nval = (jy_hi - jy_lo) * rw;
+#pragma unroll
+      for (int q = 0; q < kStage; ++q) {
+        const int i = t + q * NT;
+        if (i < nval) {
+          const int jy = jy_lo + i / rw, r = r_lo + i % rw;
+          st_soff[q * NT + t] = (unsigned)(8 * (jy * S + r));
+          st_goff[q * NT + t] = 3 * G.px * (y0 - 1 + jy) + 3 * (x0 - 1) + r;
+          ncnt = q + 1;
         }
       }
-      double* odst = Oc + ((k + kRing) % kRing) * OS;
-      const bool lin = k >= 0 && k < G.nz;
-      const double* osrc = P.occ + layer_stride * (lin ? k : 0) + (x0 - 1);
-      for (int jy = warp; jy < wy; jy += NT / 32) {
-        const int ey = y0 - 1 + jy;
-        if (ey < 0 || ey >= G.ny) continue;
-        for (int j = e_lo + lane; j < e_hi; j += 32) {
-          if (lin) cp_async8(odst + jy * wx + j, osrc + (long long)G.nx * ey + j);
-          else odst[jy * wx + j] = 0.0;
-        }
+    }
+    unsigned ooff = 0u;
+    int oeoff = 0;
+    bool has_occ = false;
+    {
+      const int ew = e_hi - e_lo;
+      const int ey_lo = max(0, 1 - y0), ey_hi = min(wy, G.ny - y0 + 1);
+      if (t < (ey_hi - ey_lo) * ew) {
+        const int jy = ey_lo + t / ew, j = e_lo + t % ew;
+        ooff = (unsigned)(8 * (jy * wx + j));
+        oeoff = G.nx * (y0 - 1 + jy) + (x0 - 1) + j;
+        has_occ = true;
+      }
+    }
+    const unsigned up_s = (unsigned)__cvta_generic_to_shared(Up), oc_s = (unsigned)__cvta_generic_to_shared(Oc);
+
+    // stage node plane k and occupancy layer k (zero-filled outside the grid)
+    auto load_layer = [&](int k) {
+      const int sl = (k + kRing) % kRing;
+      if (k >= 0 && k < G.pz) {
+        const double* src = P.u + plane_stride * k;
+        const unsigned base = up_s + (unsigned)(8 * sl * PS);
+#pragma unroll
+        for (int q = 0; q < kStage; ++q)
+          if (q < ncnt) cp_async8_s(base + st_soff[q * NT + t], src + st_goff[q * NT + t]);
+      } else {  // halo plane above / below the grid (first / last piece only)
+        double* dst = Up + sl * PS;
+#pragma unroll
+        for (int q = 0; q < kStage; ++q)
+          if (q < ncnt) dst[st_soff[q * NT + t] / 8] = 0.0;
+      }
+      if (has_occ) {
+        if (k >= 0 && k < G.nz) cp_async8_s(oc_s + (unsigned)(8 * sl * OS) + ooff, P.occ + layer_stride * k + oeoff);
+        else Oc[sl * OS + ooff / 8] = 0.0;
       }
       cp_async_commit();
     };
@@ -309,7 +345,8 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
 
 static size_t matvec_smem(int nt, int wx, int wy) {
   const int PS = (wy + 1) * plane_row_stride(wx);
-  return sizeof(double) * (kRing * (size_t)PS + kRing * (size_t)wx * wy + 2 * 9 * (size_t)(nt + kXcPad) + nt / 32 + 1);
+  return sizeof(double) * (kRing * (size_t)PS + kRing * (size_t)wx * wy + 2 * 9 * (size_t)(nt + kXcPad) + nt / 32 + 1) +
+         2 * sizeof(int) * kStage * (size_t)nt;
 }
 
 static int ctas_per_sm(int nt) { return nt == 256 ? 2 : 1; }
