@@ -126,8 +126,8 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
   double* Xc = Oc + kRing * OS;       // [2][NT + kXcPad][9] face exchange
   const int XS = 9 * (NT + kXcPad);
   double* red = Xc + 2 * XS;
-  unsigned* st_soff = reinterpret_cast<unsigned*>(red + NT / 32 + 1);  // [kStage][NT] staging lists
-  int* st_goff = reinterpret_cast<int*>(st_soff + kStage * NT);
+  // [kStage][NT] staging lists: (smem byte offset, in-plane global byte offset)
+  int2* st_list = reinterpret_cast<int2*>(red + NT / 32 + 1);
 
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
@@ -189,8 +189,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
         const int i = t + q * NT;
         if (i < nval) {
           const int jy = jy_lo + i / rw, r = r_lo + i % rw;
-          st_soff[q * NT + t] = (unsigned)(8 * (jy * S + r));
-          st_goff[q * NT + t] = 3 * G.px * (y0 - 1 + jy) + 3 * (x0 - 1) + r;
+          st_list[q * NT + t] = make_int2(8 * (jy * S + r), 8 * (3 * G.px * (y0 - 1 + jy) + 3 * (x0 - 1) + r));
           ncnt = q + 1;
         }
       }
@@ -210,20 +209,22 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
     }
     const unsigned up_s = (unsigned)__cvta_generic_to_shared(Up), oc_s = (unsigned)__cvta_generic_to_shared(Oc);
 
-    // stage node plane k and occupancy layer k (zero-filled outside the grid)
-    auto load_layer = [&](int k) {
-      const int sl = (k + kRing) % kRing;
+    // stage node plane k and occupancy layer k into ring slot sl (zero-filled outside the grid)
+    auto load_layer = [&](int k, int sl) {
       if (k >= 0 && k < G.pz) {
-        const double* src = P.u + plane_stride * k;
+        const char* src = reinterpret_cast<const char*>(P.u + plane_stride * k);
         const unsigned base = up_s + (unsigned)(8 * sl * PS);
 #pragma unroll
         for (int q = 0; q < kStage; ++q)
-          if (q < ncnt) cp_async8_s(base + st_soff[q * NT + t], src + st_goff[q * NT + t]);
+          if (q < ncnt) {
+            const int2 e = st_list[q * NT + t];
+            cp_async8_s(base + (unsigned)e.x, src + e.y);
+          }
       } else {  // halo plane above / below the grid (first / last piece only)
         double* dst = Up + sl * PS;
 #pragma unroll
         for (int q = 0; q < kStage; ++q)
-          if (q < ncnt) dst[st_soff[q * NT + t] / 8] = 0.0;
+          if (q < ncnt) dst[st_list[q * NT + t].x / 8] = 0.0;
       }
       if (has_occ) {
         if (k >= 0 && k < G.nz) cp_async8_s(oc_s + (unsigned)(8 * sl * OS) + ooff, P.occ + layer_stride * k + oeoff);
@@ -233,8 +234,8 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
     };
 
     const int j00 = ty * S + 3 * tx;
-    auto gather_face = [&](int k, double (&f)[12]) {
-      const double* pl = Up + ((k + kRing) % kRing) * PS + j00;
+    auto gather_face = [&](int sl, double (&f)[12]) {
+      const double* pl = Up + sl * PS + j00;
   #pragma unroll
       for (int b = 0; b < 4; ++b)
   #pragma unroll
@@ -249,10 +250,12 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
     double* yrow = P.y + 3 * own_node;
     const uint8_t* frow = MASKOUT ? P.fixed + own_node : nullptr;
 
-    auto step = [&](int k, const double (&bot)[12], double (&top)[12]) {
-      if (k + kAhead <= kz1 && !(P.debug & 2)) load_layer(k + kAhead);
+    // sk = ring slot of plane / layer k; plane k+1 sits in sk+1, plane k+kAhead in sk-1 (mod kRing)
+    auto step = [&](int k, int sk, const double (&bot)[12], double (&top)[12]) {
+      const int sk1 = sk == kRing - 1 ? 0 : sk + 1, skl = sk == 0 ? kRing - 1 : sk - 1;
+      if (k + kAhead <= kz1 && !(P.debug & 2)) load_layer(k + kAhead, skl);
       else cp_async_commit();  // keep one group per step
-      gather_face(k + 1, top);
+      gather_face(sk1, top);
       double own_next[3];
       if (DOT) {
         own_next[0] = top[9];
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
         own_next[2] = top[11];
       }
       xy_forward(top);
-      const double occ_e = Oc[((k + kRing) % kRing) * OS + (active ? t : 0)];
+      const double occ_e = Oc[sk * OS + (active ? t : 0)];
       double c[24];
   #pragma unroll
       for (int i = 0; i < 12; ++i) {
@@ -316,23 +319,27 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
       }
     };
 
+    const int s0 = (kz0 - 1 + kRing) % kRing;  // slot of the first staged plane kz0 - 1
     for (int j = 0; j < kAhead; ++j) {
-      if (kz0 - 1 + j <= kz1) load_layer(kz0 - 1 + j);
+      if (kz0 - 1 + j <= kz1) load_layer(kz0 - 1 + j, (s0 + j) % kRing);
       else cp_async_commit();
     }
     cp_async_wait_group<kAhead - 2>();
     __syncthreads();
     double fa[12], fb[12];
-    gather_face(kz0 - 1, fa);
+    gather_face(s0, fa);
     if (DOT) {
       own[0] = fa[9];
       own[1] = fa[10];
       own[2] = fa[11];
     }
     xy_forward(fa);
+    int sk = s0;
     for (int k = kz0 - 1; k < kz1; k += 2) {
-      step(k, fa, fb);
-      if (k + 1 < kz1) step(k + 1, fb, fa);
+      step(k, sk, fa, fb);
+      sk = sk == kRing - 1 ? 0 : sk + 1;
+      if (k + 1 < kz1) step(k + 1, sk, fb, fa);
+      sk = sk == kRing - 1 ? 0 : sk + 1;
     }
   }
   if (DOT) {
