@@ -1,7 +1,9 @@
 // extern "C" boundary of libtopovox_b200.so (declarations: include/topovox_b200.h).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/topovox_b200.h"
@@ -286,13 +288,14 @@ int tvb_matvec_host(int nx, int ny, int nz, const double* h_mh45, const double* 
   const int K = std::max(1, std::min(slabs > 0 ? slabs : 6, g.pz / 2));
 
   struct Pipe {
-    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaStream_t h2d = nullptr, d2h = nullptr, comp = nullptr;
     cudaEvent_t start = nullptr, in[64], done[64], end = nullptr;
   };
   static thread_local Pipe P;
   if (P.h2d == nullptr) {
     cudaStreamCreateWithFlags(&P.h2d, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&P.d2h, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&P.comp, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&P.start, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&P.end, cudaEventDisableTiming);
     for (int k = 0; k < 64; ++k) {
@@ -305,6 +308,7 @@ int tvb_matvec_host(int nx, int ny, int nz, const double* h_mh45, const double* 
   cudaEventRecord(P.start, s);
   cudaStreamWaitEvent(P.h2d, P.start, 0);
   cudaStreamWaitEvent(P.d2h, P.start, 0);
+  cudaStreamWaitEvent(P.comp, P.start, 0);
   int loaded = 0;  // input planes [0, loaded) issued
   for (int k = 0; k < KK; ++k) {
     const int z0 = (int)((long long)g.pz * k / KK), z1 = (int)((long long)g.pz * (k + 1) / KK);
@@ -320,7 +324,7 @@ int tvb_matvec_host(int nx, int ny, int nz, const double* h_mh45, const double* 
       loaded = need;
     }
     cudaEventRecord(P.in[k], P.h2d);
-    cudaStreamWaitEvent(s, P.in[k], 0);
+    cudaStreamWaitEvent(P.comp, P.in[k], 0);
     MatvecParams mp{};
     mp.g = g;
     mp.u = du;
@@ -330,9 +334,9 @@ int tvb_matvec_host(int nx, int ny, int nz, const double* h_mh45, const double* 
     mp.mask_out = (flags & TVB_MASK_OUT) ? 1 : 0;
     mp.zlo = z0;
     mp.zhi = z1;
-    const int st = check(launch_matvec(pl, mp, M, s));
+    const int st = check(launch_matvec(pl, mp, M, P.comp));
     if (st) return st;
-    cudaEventRecord(P.done[k], s);
+    cudaEventRecord(P.done[k], P.comp);
     cudaStreamWaitEvent(P.d2h, P.done[k], 0);
     cudaMemcpyAsync(h_out + pdoubles * z0, dy + pdoubles * z0, sizeof(double) * pdoubles * (z1 - z0),
                     cudaMemcpyDeviceToHost, P.d2h);
