@@ -211,7 +211,7 @@ cudaError_t launch_block_basis(const Agglo& A, const double* occ, const uint8_t*
 // restriction: yc_B = S_B^T [sum y~ ; sum r x y~] over structural nodes of the
 // closed box, y~ = y with fixed DOFs zeroed. One CTA per block, fixed order.
 // ---------------------------------------------------------------------------
-constexpr int kRestrictThreads = 256;
+constexpr int kRestrictThreads = 128;  // measured best at C4 (256 threads: +5 us per restriction)
 
 // BS > 0: compile-time block size (the closed box has at most (BS+1)^3 nodes;
 // positions outside a clipped boundary box are skipped); BS = 0: runtime size.
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kRestrictThreads) k_restrict(Agglo A, const ui
   const int npos = PX * PY * PZ;
   double acc[6] = {0, 0, 0, 0, 0, 0};
   // up to kNodes nodes per thread per step, all their loads issued before use
-  constexpr int kNodes = 3;
+  constexpr int kNodes = 4;
   for (int i0 = threadIdx.x; i0 < npos; i0 += kNodes * blockDim.x) {
     uint8_t fl[kNodes];
     double w[kNodes][3];
