@@ -245,7 +245,6 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
     double carry[12];
   #pragma unroll
     for (int i = 0; i < 12; ++i) carry[i] = 0.0;
-    double own[3] = {0.0, 0.0, 0.0};  // u at the owned node of the current plane (dot epilogue)
     const long long own_node = G.node(min(x0 + tx, G.px - 1), min(y0 + ty, G.py - 1), kz0);
     double* yrow = P.y + 3 * own_node;
     const uint8_t* frow = MASKOUT ? P.fixed + own_node : nullptr;
@@ -256,12 +255,6 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
       if (k + kAhead <= kz1 && !(P.debug & 2)) load_layer(k + kAhead, skl);
       else cp_async_commit();  // keep one group per step
       gather_face(sk1, top);
-      double own_next[3];
-      if (DOT) {
-        own_next[0] = top[9];
-        own_next[1] = top[10];
-        own_next[2] = top[11];
-      }
       xy_forward(top);
       const double occ_e = Oc[sk * OS + (active ? t : 0)];
       double c[24];
@@ -306,16 +299,13 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
             double w = ((fx >> a) & 1) ? 0.0 : v[a];
             if (P.accumulate) w += yrow[a];
             if (!(P.debug & 4)) yrow[a] = w;
-            if (DOT) dot = fma(own[a], w, dot);
+            // dot epilogue: u at the owned node, re-read from the staged plane k
+            // (its slot is only refilled after this step's barrier)
+            if (DOT) dot = fma(Up[sk * PS + j00 + S + 3 + a], w, dot);
           }
         }
         yrow += plane_stride;
         if (MASKOUT) frow += (long long)G.px * G.py;
-      }
-      if (DOT) {
-        own[0] = own_next[0];
-        own[1] = own_next[1];
-        own[2] = own_next[2];
       }
     };
 
@@ -328,11 +318,6 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
     __syncthreads();
     double fa[12], fb[12];
     gather_face(s0, fa);
-    if (DOT) {
-      own[0] = fa[9];
-      own[1] = fa[10];
-      own[2] = fa[11];
-    }
     xy_forward(fa);
     int sk = s0;
     for (int k = kz0 - 1; k < kz1; k += 2) {
