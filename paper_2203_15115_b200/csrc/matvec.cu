@@ -281,6 +281,14 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
   #pragma unroll
         for (int i = 0; i < 9; ++i) xs[9 * t + i] = face[i];  // nodes (0,0), (1,0), (0,1)
       }
+      // dot epilogue operand: u at the owned node, read from staged plane k
+      // BEFORE the barrier (after it, a faster thread may already refill the
+      // slot with plane k + kRing)
+      double uo[3];
+      if (DOT) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) uo[a] = Up[sk * PS + j00 + S + 3 + a];
+      }
       cp_async_wait_group<kAhead - 2>();  // plane k+2 (and occupancy k+2) landed
       if (!(P.debug & 1)) __syncthreads();
       if (out) {
@@ -299,9 +307,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
             double w = ((fx >> a) & 1) ? 0.0 : v[a];
             if (P.accumulate) w += yrow[a];
             if (!(P.debug & 4)) yrow[a] = w;
-            // dot epilogue: u at the owned node, re-read from the staged plane k
-            // (its slot is only refilled after this step's barrier)
-            if (DOT) dot = fma(Up[sk * PS + j00 + S + 3 + a], w, dot);
+            if (DOT) dot = fma(uo[a], w, dot);
           }
         }
         yrow += plane_stride;
