@@ -347,7 +347,7 @@ template <int BS>
 __global__ void __launch_bounds__(kProlongThreads) k_prolong(Agglo A, const uint8_t* __restrict__ nflags,
                                                  const double* __restrict__ cen, const double* __restrict__ nu,
                                                  double* __restrict__ out, const double* __restrict__ z,
-                                                 const SolverState* st, int mode) {
+                                                 double* __restrict__ x, const SolverState* st, int mode) {
   const Grid& G = A.g;
   const unsigned n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= (unsigned)G.nn) return;
@@ -394,6 +394,11 @@ __global__ void __launch_bounds__(kProlongThreads) k_prolong(Agglo A, const uint
       if ((fl >> a) & 1) v[a] = 0.0;
   }
   const double beta = mode == 1 ? st->beta : 0.0;
+  if (mode == 1 && x != nullptr) {  // deferred x += alpha p_old of this iteration (p_old = o)
+    const double alpha = st->alpha;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) x[3ull * n + a] = fma(alpha, o[a], x[3ull * n + a]);
+  }
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const double r = mode == 0 ? v[a] : (mode == 1 ? fma(beta, o[a], zv[a]) - v[a] : zv[a] - v[a]);
@@ -402,12 +407,12 @@ __global__ void __launch_bounds__(kProlongThreads) k_prolong(Agglo A, const uint
 }
 
 cudaError_t launch_prolong(const Agglo& A, const uint8_t* nflags, DeflData D, const double* nu, double* out,
-                           const double* z, const void* state, int mode, cudaStream_t s) {
+                           const double* z, const void* state, int mode, cudaStream_t s, double* x) {
   const unsigned g = (unsigned)((A.g.nn + kProlongThreads - 1) / kProlongThreads);
   const SolverState* st = (const SolverState*)state;
-  if (A.b == 8) k_prolong<8><<<g, kProlongThreads, 0, s>>>(A, nflags, D.cen, nu, out, z, st, mode);
-  else if (A.b == 4) k_prolong<4><<<g, kProlongThreads, 0, s>>>(A, nflags, D.cen, nu, out, z, st, mode);
-  else k_prolong<0><<<g, kProlongThreads, 0, s>>>(A, nflags, D.cen, nu, out, z, st, mode);
+  if (A.b == 8) k_prolong<8><<<g, kProlongThreads, 0, s>>>(A, nflags, D.cen, nu, out, z, x, st, mode);
+  else if (A.b == 4) k_prolong<4><<<g, kProlongThreads, 0, s>>>(A, nflags, D.cen, nu, out, z, x, st, mode);
+  else k_prolong<0><<<g, kProlongThreads, 0, s>>>(A, nflags, D.cen, nu, out, z, x, st, mode);
   return cudaGetLastError();
 }
 

@@ -58,8 +58,10 @@ cudaError_t launch_restrict(const Agglo& A, const uint8_t* nflags, DeflData D, c
 cudaError_t launch_block_nu(const Agglo& A, DeflData D, const double* mu, double* nu, cudaStream_t s,
                             const int* stop = nullptr);
 // mode 0: out = W nu ; mode 1: out(=p) = z + beta*p - W nu (beta/done from solver state) ; mode 2: out = z - W nu
+// x (mode 1, optional): also x += alpha p_old (the solver's deferred x update;
+// alpha from the solver state)
 cudaError_t launch_prolong(const Agglo& A, const uint8_t* nflags, DeflData D, const double* nu, double* out,
-                           const double* z, const void* state, int mode, cudaStream_t s);
+                           const double* z, const void* state, int mode, cudaStream_t s, double* x = nullptr);
 // coarse operator probing helpers
 cudaError_t launch_probe_nu(const Agglo& A, DeflData D, int color, int j, double* nu, cudaStream_t s);
 cudaError_t launch_probe_scatter(const Agglo& A, int color, int j, const double* yc, double* Eb, cudaStream_t s);

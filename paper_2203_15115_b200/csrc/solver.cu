@@ -253,7 +253,7 @@ int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
     cudaError_t e = cudaSuccess;
     if (!(skip & 1) && (e = matvec(W.p, W.q, true, stop)) != cudaSuccess) return e;
     if (!(skip & 2) &&
-        (e = launch_pcg_update(nd, P.x, W.r, W.z, W.p, W.q, W.inv_d, W.st, W.partials,
+        (e = launch_pcg_update(nd, defl ? nullptr : P.x, W.r, W.z, W.p, W.q, W.inv_d, W.st, W.partials,
                                W.partials + 2 * kMaxReduceCtas, plan.nblocks(), s)) != cudaSuccess)
       return e;
     if (defl) {
@@ -267,7 +267,8 @@ int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
       }
       if (skip & 32) return cudaSuccess;
       if ((e = launch_block_nu(A, D, W.mu, W.nu, s, stop)) != cudaSuccess) return e;
-      return launch_prolong(A, P.nflags, D, W.nu, W.p, W.z, W.st, 1, s);
+      // p = z + beta p - W nu, and the deferred x += alpha p_old of this iteration
+      return launch_prolong(A, P.nflags, D, W.nu, W.p, W.z, W.st, 1, s, P.x);
     }
     return launch_pcg_pupdate(nd, W.p, W.z, W.st, s);
   };
@@ -283,8 +284,8 @@ int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
       cudaEventRecord(ev[0], s);
       matvec(W.p, W.q, true, stop);
       cudaEventRecord(ev[1], s);
-      launch_pcg_update(nd, P.x, W.r, W.z, W.p, W.q, W.inv_d, W.st, W.partials, W.partials + 2 * kMaxReduceCtas,
-                        plan.nblocks(), s);
+      launch_pcg_update(nd, defl ? nullptr : P.x, W.r, W.z, W.p, W.q, W.inv_d, W.st, W.partials,
+                        W.partials + 2 * kMaxReduceCtas, plan.nblocks(), s);
       cudaEventRecord(ev[2], s);
       if (defl) {
         matvec(W.z, W.t, false, stop);
@@ -295,7 +296,7 @@ int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
         else launch_dense_gemv(6 * A.nb, P.coarse, W.yc, W.mu, stop, s);
         cudaEventRecord(ev[5], s);
         launch_block_nu(A, D, W.mu, W.nu, s, stop);
-        launch_prolong(A, P.nflags, D, W.nu, W.p, W.z, W.st, 1, s);
+        launch_prolong(A, P.nflags, D, W.nu, W.p, W.z, W.st, 1, s, P.x);
       } else {
         launch_pcg_pupdate(nd, W.p, W.z, W.st, s);
         for (int k = 3; k < 6; ++k) cudaEventRecord(ev[k], s);
@@ -344,6 +345,8 @@ int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
       return kStatusCuda;
     }
   }
+  // the stopping iteration's x += alpha p rode on its (skipped) prolongation
+  if (defl && hst.iter > 0) TVB_CK(launch_x_finish(nd, P.x, W.p, W.st, s));
   R.iterations = hst.iter;
   R.residual = hst.res;
   if (hst.done == 2) {

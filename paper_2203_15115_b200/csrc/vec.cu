@@ -97,8 +97,7 @@ __global__ void k_pcg_update(long long n, double* x, double* r, double* z, const
   const long long lo = blockIdx.x * per, hi = min(n, lo + per);
   double rr = 0.0, rz = 0.0;
   for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    const double pi = p[i];
-    x[i] = fma(alpha, pi, x[i]);
+    if (x != nullptr) x[i] = fma(alpha, p[i], x[i]);
     const double ri = fma(-alpha, q[i], r[i]);
     r[i] = ri;
     const double zi = inv_d[i] * ri;
@@ -132,6 +131,9 @@ __global__ void k_pcg_update(long long n, double* x, double* r, double* z, const
 // thread streams two double2 of every vector per step, so ~12 independent
 // 16-byte loads are in flight per thread. Identical arithmetic per element;
 // the partial sums run in a different (still fixed) order.
+// WX = false: x is not touched (the deflated solver folds x += alpha p into
+// the prolongation, which reads p anyway).
+template <bool WX>
 __global__ void __launch_bounds__(256) k_pcg_update_v2(long long n, double* __restrict__ x, double* __restrict__ r,
                                                        double* __restrict__ z, const double* __restrict__ p,
                                                        const double* __restrict__ q,
@@ -167,14 +169,16 @@ __global__ void __launch_bounds__(256) k_pcg_update_v2(long long n, double* __re
   const double2* d2 = reinterpret_cast<const double2*>(inv_d);
   double rr = 0.0, rz = 0.0;
   auto one = [&](double2 pi, double2 xi, double2 qi, double2 ri, double2 di, long long i) {
-    xi.x = fma(alpha, pi.x, xi.x);
-    xi.y = fma(alpha, pi.y, xi.y);
+    if (WX) {
+      xi.x = fma(alpha, pi.x, xi.x);
+      xi.y = fma(alpha, pi.y, xi.y);
+      __stcs(x2 + i, xi);  // x and r are next read one iteration later: evict first
+    }
     ri.x = fma(-alpha, qi.x, ri.x);
     ri.y = fma(-alpha, qi.y, ri.y);
     double2 zi;
     zi.x = di.x * ri.x;
     zi.y = di.y * ri.y;
-    __stcs(x2 + i, xi);  // x and r are next read one iteration later: evict first
     __stcs(r2 + i, ri);
     z2[i] = zi;
     rr = fma(ri.x, ri.x, rr);
@@ -185,16 +189,17 @@ __global__ void __launch_bounds__(256) k_pcg_update_v2(long long n, double* __re
   long long i = lo + threadIdx.x;
   for (; i + blockDim.x < hi; i += 2 * blockDim.x) {
     const long long j = i + blockDim.x;
-    const double2 pa = p2[i], pb = p2[j], xa = x2[i], xb = x2[j];
+    const double2 pa = WX ? p2[i] : double2{}, pb = WX ? p2[j] : double2{};
+    const double2 xa = WX ? x2[i] : double2{}, xb = WX ? x2[j] : double2{};
     const double2 qa = q2[i], qb = q2[j], ra = r2[i], rb = r2[j];
     const double2 da = __ldg(d2 + i), db = __ldg(d2 + j);
     one(pa, xa, qa, ra, da, i);
     one(pb, xb, qb, rb, db, j);
   }
-  if (i < hi) one(p2[i], x2[i], q2[i], r2[i], __ldg(d2 + i), i);
+  if (i < hi) one(WX ? p2[i] : double2{}, WX ? x2[i] : double2{}, q2[i], r2[i], __ldg(d2 + i), i);
   if ((n & 1) && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {  // odd tail element
     const long long k = n - 1;
-    x[k] = fma(alpha, p[k], x[k]);
+    if (WX) x[k] = fma(alpha, p[k], x[k]);
     const double rk = fma(-alpha, q[k], r[k]);
     r[k] = rk;
     const double zk = inv_d[k] * rk;
@@ -223,6 +228,17 @@ __global__ void __launch_bounds__(256) k_pcg_update_v2(long long n, double* __re
       st->rz = t[1];
     }
   });
+}
+
+__global__ void k_x_finish(long long n, double* x, const double* p, const SolverState* st) {
+  const double alpha = st->alpha;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    x[i] = fma(alpha, p[i], x[i]);
+}
+
+cudaError_t launch_x_finish(long long n, double* x, const double* p, const SolverState* st, cudaStream_t s) {
+  k_x_finish<<<reduce_grid(n) * 4, 256, 0, s>>>(n, x, p, st);
+  return cudaGetLastError();
 }
 
 // plain PCG direction update p = z + beta p
@@ -326,11 +342,13 @@ cudaError_t launch_dot(const double* a, const double* b, const double* w, long l
 cudaError_t launch_pcg_update(long long n, double* x, double* r, double* z, const double* p, const double* q,
                               const double* inv_d, SolverState* st, double* partials, const double* pq_parts,
                               int n_parts, cudaStream_t s) {
-  const bool vec16 = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(r) |
+  const bool vec16 = (((x ? reinterpret_cast<uintptr_t>(x) : 0) | reinterpret_cast<uintptr_t>(r) |
                        reinterpret_cast<uintptr_t>(z) | reinterpret_cast<uintptr_t>(p) |
                        reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(inv_d)) & 15) == 0;
-  if (vec16) {
-    k_pcg_update_v2<<<reduce_grid(n), 256, 0, s>>>(n, x, r, z, p, q, inv_d, st, partials, pq_parts, n_parts);
+  if (vec16 && x != nullptr) {
+    k_pcg_update_v2<true><<<reduce_grid(n), 256, 0, s>>>(n, x, r, z, p, q, inv_d, st, partials, pq_parts, n_parts);
+  } else if (vec16) {
+    k_pcg_update_v2<false><<<reduce_grid(n), 256, 0, s>>>(n, x, r, z, p, q, inv_d, st, partials, pq_parts, n_parts);
   } else {
     if (pq_parts != nullptr) k_finalize_pq<<<1, 256, 0, s>>>(pq_parts, n_parts, st);
     k_pcg_update<<<reduce_grid(n), 256, 0, s>>>(n, x, r, z, p, q, inv_d, st, partials);

@@ -34,6 +34,9 @@ cudaError_t launch_dot(const double* a, const double* b, const double* w, long l
 cudaError_t launch_pcg_update(long long n, double* x, double* r, double* z, const double* p, const double* q,
                               const double* inv_d, SolverState* st, double* partials, const double* pq_parts,
                               int n_parts, cudaStream_t s);
+// x += alpha p with alpha from the solver state: the last iteration's deferred
+// x update (its prolongation, which carries it, is skipped once done is set)
+cudaError_t launch_x_finish(long long n, double* x, const double* p, const SolverState* st, cudaStream_t s);
 cudaError_t launch_pcg_pupdate(long long n, double* p, const double* z, const SolverState* st, cudaStream_t s);
 cudaError_t launch_finalize_pq(const double* partials, int nparts, SolverState* st, cudaStream_t s);
 cudaError_t launch_pcg_init(long long n, const double* f, double* r, double* z, const double* inv_d,
