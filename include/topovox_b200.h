@@ -171,6 +171,10 @@ typedef struct tvb_coarse_nd {
   unsigned long long* d_ctl;  /* [3] next item, CTAs exited, epoch; zero-initialised once */
   const double* d_factor;   /* the single allocation holding G, B, ZT (L2 persistence window) */
   size_t factor_bytes;
+  /* multi-RHS scratch: column c of d_fS / d_cU / d_fT at + c * fs_ld / cu_ld / ft_ld;
+     max_cols columns allocated (solves of more RHS run in groups of max_cols) */
+  long long fs_ld, cu_ld, ft_ld;
+  int max_cols;
 } tvb_coarse_nd;
 int tvb_coarse_nd_solve(const tvb_coarse_nd* nd, const double* d_y, double* d_x, void* stream);
 
@@ -206,6 +210,18 @@ typedef struct tvb_pcg_desc {
 
 size_t tvb_pcg_ws_bytes(int nx, int ny, int nz, int block);
 int tvb_pcg_solve(tvb_pcg_desc* desc, void* stream);
+
+/* Multi-RHS batching: nrhs (<= 8) independent solves
+ * K x_c = f_c against the operator / deflation space of `desc` (its d_f, d_x
+ * and outputs are ignored). One CUDA graph iterates all RHS; the coarse solve
+ * reads the factor once per iteration for all of them. Each RHS keeps its own
+ * stopping test and iteration count, and its result is bitwise equal to
+ * tvb_pcg_solve on it alone. Per-RHS outputs: h_iterations, h_residuals,
+ * h_status (0 / NoConvergence / Singular ...). Returns the first failing
+ * per-RHS status. d_ws >= tvb_pcg_batch_ws_bytes(). */
+size_t tvb_pcg_batch_ws_bytes(int nx, int ny, int nz, int block, int nrhs);
+int tvb_pcg_solve_batch(tvb_pcg_desc* desc, int nrhs, const double* const* h_d_f, double* const* h_d_x,
+                        int* h_iterations, double* h_residuals, int* h_status, void* stream);
 
 /* a9/a10/a11: element state -- replaces batch_element_state (fea.py:302-309)
  * plus the compliance sensitivity T_J and the p-norm sums

@@ -35,6 +35,8 @@ class CoarseND(ctypes.Structure):
         ("d_perm", P),
         ("d_items", P), ("n_items", c_int), ("d_rel", P), ("d_cnt", P), ("d_ctl", P),
         ("d_factor", P), ("factor_bytes", c_size_t),
+        ("fs_ld", ctypes.c_longlong), ("cu_ld", ctypes.c_longlong), ("ft_ld", ctypes.c_longlong),
+        ("max_cols", c_int),
     ]
 
 
@@ -76,6 +78,8 @@ _SIGS = {
     "tvb_coarse_nd_solve": (c_int, [ctypes.POINTER(CoarseND), P, P, P]),
     "tvb_pcg_ws_bytes": (c_size_t, [c_int, c_int, c_int, c_int]),
     "tvb_pcg_solve": (c_int, [ctypes.POINTER(PcgDesc), P]),
+    "tvb_pcg_batch_ws_bytes": (c_size_t, [c_int, c_int, c_int, c_int, c_int]),
+    "tvb_pcg_solve_batch": (c_int, [ctypes.POINTER(PcgDesc), c_int, P, P, P, P, P, P]),
     "tvb_elem_ws_bytes": (c_size_t, [c_int, c_int, c_int]),
     "tvb_element_state": (c_int, [c_int, c_int, c_int, c_double, c_double, c_double, P, P, P, P, P, P, c_int, P, P,
                                   c_size_t, P]),

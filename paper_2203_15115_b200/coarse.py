@@ -67,6 +67,9 @@ FLOW_MIN_DOFS = 48000
 WARPS_IN_FLIGHT = int(os.environ.get("TVB_ND_WARPS", "2368"))
 #: dynamic shared memory per CTA (B200: 227 KB opt-in)
 SMEM_MAX = 227 * 1024
+#: right-hand sides per coarse-solve launch (coarse.cu kCoarseMaxCols); the
+#: scratch vectors fS / cU / fT carry this many columns
+MAX_COLS = 4
 #: resident 256-thread CTAs on the GPU (148 SMs x 8): one wave of solve items
 CTA_SLOTS = int(os.environ.get("TVB_ND_SLOTS", "1184"))
 #: index plans of the numeric factorisation, keyed by (block grid, leaf, top, device)
@@ -411,9 +414,11 @@ class NDCoarseSolver:
         self.tptr = torch.from_numpy(tptr.astype(np.int32)).to(dev)
         self.tidx = torch.from_numpy(np.concatenate([ti, [0]]).astype(np.int32)).to(dev)
         n_c = 6 * self.nb
-        self.fS = torch.zeros(n_c + 1, dtype=torch.float64, device=dev)   # indexed by ND dof
-        self.cU = torch.zeros(n_cu + 1, dtype=torch.float64, device=dev)
-        self.fT = torch.zeros(self.n_top + 1, dtype=torch.float64, device=dev)
+        # per-RHS scratch columns (multi-RHS solves, coarse.cu ColSet)
+        self.max_cols = MAX_COLS
+        self.fS = torch.zeros(MAX_COLS, n_c + 1, dtype=torch.float64, device=dev)   # indexed by ND dof
+        self.cU = torch.zeros(MAX_COLS, n_cu + 1, dtype=torch.float64, device=dev)
+        self.fT = torch.zeros(MAX_COLS, self.n_top + 1, dtype=torch.float64, device=dev)
         self.perm = torch.from_numpy(self.perm_host.astype(np.int32)).to(dev)
         # work items per bottom height: (node, row0, row1); fwd rows = u (length s),
         # bwd rows = s (length s + u); 8 / wpr rows per 256-thread CTA
@@ -580,6 +585,8 @@ class NDCoarseSolver:
             d.d_items, d.n_items, d.d_rel = ptr(self.items), self.n_items, ptr(self.rel)
             d.d_cnt, d.d_ctl = ptr(self.cnt), ptr(self.ctl)
         d.d_factor, d.factor_bytes = ptr(self.factor), self.bytes
+        d.fs_ld, d.cu_ld, d.ft_ld = self.fS.shape[1], self.cU.shape[1], self.fT.shape[1]
+        d.max_cols = self.max_cols
         return d
 
     def solve_device(self, y, x):

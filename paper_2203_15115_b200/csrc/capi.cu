@@ -141,6 +141,10 @@ static CoarseNDDev coarse_nd_dev(const tvb_coarse_nd* d) {
   D.rel = d->d_rel;
   D.cnt = d->d_cnt;
   D.ctl = d->d_ctl;
+  D.fs_ld = d->fs_ld;
+  D.cu_ld = d->cu_ld;
+  D.ft_ld = d->ft_ld;
+  D.max_cols = d->max_cols > 0 ? d->max_cols : 1;
   return D;
 }
 
@@ -512,12 +516,10 @@ size_t tvb_pcg_ws_bytes(int nx, int ny, int nz, int block) {
   return pcg_ws_bytes(make_grid(nx, ny, nz), block);
 }
 
-int tvb_pcg_solve(tvb_pcg_desc* d, void* stream) {
-  if (!d || bad_dims(d->nx, d->ny, d->nz) || !d->h_mh45 || !d->h_kdiag3 || !d->d_occ || !d->d_nflags || !d->d_f ||
-      !d->d_x || !d->d_ws)
+static int pcg_problem(const tvb_pcg_desc* d, PcgProblem& P) {
+  if (!d || bad_dims(d->nx, d->ny, d->nz) || !d->h_mh45 || !d->h_kdiag3 || !d->d_occ || !d->d_nflags || !d->d_ws)
     return kStatusBadArg;
   if (!(d->tol > 0.0) || d->max_iters < 1) return kStatusBadArg;
-  PcgProblem P{};
   P.g = make_grid(d->nx, d->ny, d->nz);
   P.h = d->h;
   if (!modal_reduce(d->h_mh45, P.modal)) return kStatusBadArg;
@@ -544,11 +546,45 @@ int tvb_pcg_solve(tvb_pcg_desc* d, void* stream) {
     P.nd_factor_bytes = d->coarse_nd->factor_bytes;
   }
   if (P.block > 0 && (!P.cen || !P.S || !P.keep)) return kStatusBadArg;
+  return kStatusOk;
+}
+
+int tvb_pcg_solve(tvb_pcg_desc* d, void* stream) {
+  PcgProblem P{};
+  if (!d || !d->d_f || !d->d_x) return kStatusBadArg;
+  if (int st = pcg_problem(d, P)) return st;
   PcgResult R;
   const int st = pcg_solve(P, R, (cudaStream_t)stream);
   d->iterations = R.iterations;
   d->residual = R.residual;
   d->fnorm = R.fnorm;
+  return st;
+}
+
+size_t tvb_pcg_batch_ws_bytes(int nx, int ny, int nz, int block, int nrhs) {
+  if (bad_dims(nx, ny, nz) || nrhs < 1 || nrhs > kPcgMaxRhs) return 0;
+  return (size_t)nrhs * pcg_ws_bytes(make_grid(nx, ny, nz), block);
+}
+
+int tvb_pcg_solve_batch(tvb_pcg_desc* d, int nrhs, const double* const* h_d_f, double* const* h_d_x,
+                        int* h_iterations, double* h_residuals, int* h_status, void* stream) {
+  if (nrhs < 1 || nrhs > kPcgMaxRhs || !h_d_f || !h_d_x) return kStatusBadArg;
+  PcgProblem P{};
+  if (int st = pcg_problem(d, P)) return st;
+  P.nrhs = nrhs;
+  for (int c = 0; c < nrhs; ++c) {
+    if (!h_d_f[c] || !h_d_x[c]) return kStatusBadArg;
+    P.fs[c] = h_d_f[c];
+    P.xs[c] = h_d_x[c];
+  }
+  PcgResult R[kPcgMaxRhs];
+  int rs[kPcgMaxRhs];
+  const int st = pcg_solve_multi(P, R, rs, (cudaStream_t)stream);
+  for (int c = 0; c < nrhs; ++c) {
+    if (h_iterations) h_iterations[c] = R[c].iterations;
+    if (h_residuals) h_residuals[c] = R[c].residual;
+    if (h_status) h_status[c] = rs[c];
+  }
   return st;
 }
 

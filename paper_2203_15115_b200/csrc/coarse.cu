@@ -39,47 +39,84 @@ namespace tvb {
 
 constexpr int kCoarseThreads = 256;
 constexpr int kCoarseWarps = kCoarseThreads / 32;
+constexpr int kRedStride = 4 * kCoarseWarps;  // per-column slice of the row-reduction scratch
 
 enum CoarseItem : int { kFwd = 0, kAsm = 1, kRows = 2, kTopGather = 3, kTopRows = 4, kBwd = 5 };
 
+// Multi-RHS: every kernel below is templated on MC, the number of right-hand
+// sides solved together (1..kCoarseMaxCols). A factor row is loaded once and
+// dotted with all MC columns; the arithmetic of each column is exactly the
+// single-column sequence (same accumulators, same order), so a column of a
+// batched solve is bitwise equal to the same vector solved alone.
+struct ColSet {
+  const double* y;   // column c at y + c * ldy (ND order)
+  long long ldy;
+  double* x;         // column c at x + c * ldx
+  long long ldx;
+  const int* stop;   // column c stopped <=> stop[c * stop_ld] != 0 (nullptr: never)
+  long long stop_ld;
+};
+
+template <int MC>
+__device__ __forceinline__ bool all_stopped(const ColSet& C) {
+  if (C.stop == nullptr) return false;
+#pragma unroll
+  for (int c = 0; c < MC; ++c)
+    if (!C.stop[c * C.stop_ld]) return false;
+  return true;
+}
+
 // Part `part` of row . vector (lane-strided over WPR warps), row streamed from
-// global memory with 8 independent loads in flight per lane.
-template <int WPR>
-__device__ __forceinline__ double part_dot(const double* __restrict__ a, const double* b, int n, int part, int lane) {
+// global memory with 8 independent loads in flight per lane; MC vectors at
+// stride ldb.
+template <int WPR, int MC>
+__device__ __forceinline__ void part_dot(const double* __restrict__ a, const double* b, int ldb, int n, int part,
+                                         int lane, double (&out)[MC]) {
   constexpr int st = 32 * WPR;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  double s[MC][4];
+#pragma unroll
+  for (int c = 0; c < MC; ++c) s[c][0] = s[c][1] = s[c][2] = s[c][3] = 0.0;
   int i = part * 32 + lane;
   for (; i + 7 * st < n; i += 8 * st) {
     double v[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] = __ldg(a + i + st * k);
-    s0 = fma(v[0], b[i], s0);
-    s1 = fma(v[1], b[i + st], s1);
-    s2 = fma(v[2], b[i + 2 * st], s2);
-    s3 = fma(v[3], b[i + 3 * st], s3);
-    s0 = fma(v[4], b[i + 4 * st], s0);
-    s1 = fma(v[5], b[i + 5 * st], s1);
-    s2 = fma(v[6], b[i + 6 * st], s2);
-    s3 = fma(v[7], b[i + 7 * st], s3);
+#pragma unroll
+    for (int c = 0; c < MC; ++c) {
+      const double* bc = b + c * ldb;
+      s[c][0] = fma(v[0], bc[i], s[c][0]);
+      s[c][1] = fma(v[1], bc[i + st], s[c][1]);
+      s[c][2] = fma(v[2], bc[i + 2 * st], s[c][2]);
+      s[c][3] = fma(v[3], bc[i + 3 * st], s[c][3]);
+      s[c][0] = fma(v[4], bc[i + 4 * st], s[c][0]);
+      s[c][1] = fma(v[5], bc[i + 5 * st], s[c][1]);
+      s[c][2] = fma(v[6], bc[i + 6 * st], s[c][2]);
+      s[c][3] = fma(v[7], bc[i + 7 * st], s[c][3]);
+    }
   }
   double v[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) v[k] = (i + st * k < n) ? __ldg(a + i + st * k) : 0.0;
 #pragma unroll
   for (int k = 0; k < 8; ++k)
-    if (i + st * k < n) s0 = fma(v[k], b[i + st * k], s0);
-  return warp_sum((s0 + s1) + (s2 + s3));
+    if (i + st * k < n)
+#pragma unroll
+      for (int c = 0; c < MC; ++c) s[c][0] = fma(v[k], b[c * ldb + i + st * k], s[c][0]);
+#pragma unroll
+  for (int c = 0; c < MC; ++c) out[c] = warp_sum((s[c][0] + s[c][1]) + (s[c][2] + s[c][3]));
 }
 
 // RPW rows at once by one warp (WPR = 1): 8 loads in flight per lane split
-// over the rows. out[q] = row q . b (full warp sum).
-template <int RPW>
-__device__ __forceinline__ void multi_dot(const double* __restrict__ a, long long n, const double* b, int lane,
-                                          double* out) {
+// over the rows. out[q][c] = row q . b_c (full warp sum).
+template <int RPW, int MC>
+__device__ __forceinline__ void multi_dot(const double* __restrict__ a, long long n, const double* b, int ldb,
+                                          int lane, double (&out)[RPW][MC]) {
   constexpr int K = 8 / RPW;
-  double s[RPW][2];
+  double s[RPW][MC][2];
 #pragma unroll
-  for (int q = 0; q < RPW; ++q) s[q][0] = s[q][1] = 0.0;
+  for (int q = 0; q < RPW; ++q)
+#pragma unroll
+    for (int c = 0; c < MC; ++c) s[q][c][0] = s[q][c][1] = 0.0;
   int i = lane;
   for (; i + (K - 1) * 32 < n; i += K * 32) {
     double w[RPW][K];
@@ -90,57 +127,83 @@ __device__ __forceinline__ void multi_dot(const double* __restrict__ a, long lon
 #pragma unroll
     for (int q = 0; q < RPW; ++q)
 #pragma unroll
-      for (int k = 0; k < K; ++k) s[q][k & 1] = fma(w[q][k], b[i + 32 * k], s[q][k & 1]);
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int c = 0; c < MC; ++c) s[q][c][k & 1] = fma(w[q][k], b[c * ldb + i + 32 * k], s[q][c][k & 1]);
   }
   for (; i < n; i += 32)
 #pragma unroll
-    for (int q = 0; q < RPW; ++q) s[q][0] = fma(__ldg(a + q * n + i), b[i], s[q][0]);
+    for (int q = 0; q < RPW; ++q) {
+      const double aq = __ldg(a + q * n + i);
 #pragma unroll
-  for (int q = 0; q < RPW; ++q) out[q] = warp_sum(s[q][0] + s[q][1]);
+      for (int c = 0; c < MC; ++c) s[q][c][0] = fma(aq, b[c * ldb + i], s[q][c][0]);
+    }
+#pragma unroll
+  for (int q = 0; q < RPW; ++q)
+#pragma unroll
+    for (int c = 0; c < MC; ++c) out[q][c] = warp_sum(s[q][c][0] + s[q][c][1]);
 }
 
 // Rows r0 .. r0 + 8*RPW/WPR - 1 (< r1) of M (row length n) dotted with the
-// shared vector v: WPR warps per row (RPW = 1) or RPW rows per warp (WPR = 1).
-// Returns the full dot to threads t < 8*RPW/WPR (row r0 + t).
-template <int WPR, int RPW>
-__device__ __forceinline__ double rows_dot(const double* __restrict__ M, long long n, const double* v, int r0, int r1,
-                                           double* red) {
+// MC shared vectors v + c*ldv: WPR warps per row (RPW = 1) or RPW rows per
+// warp (WPR = 1). Leaves the full dots in d[] of threads t < 8*RPW/WPR (row
+// r0 + t). red: MC * kRedStride doubles.
+template <int WPR, int RPW, int MC>
+__device__ __forceinline__ void rows_dot(const double* __restrict__ M, long long n, const double* v, int ldv, int r0,
+                                         int r1, double* red, double (&d)[MC]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (RPW == 1) {
     const int j = r0 + warp / WPR;
-    const double p = (j < r1) ? part_dot<WPR>(M + (long long)j * n, v, (int)n, warp % WPR, lane) : 0.0;
-    if (lane == 0) red[warp] = p;
-  } else {
-    const int j0 = r0 + warp * RPW;
-    double p[RPW];
-    if (j0 < r1) {
-      // rows past r1 re-read row r1-1 (results discarded)
-      const int jl = min(j0 + RPW, r1) - j0;
-      if (jl == RPW) {
-        multi_dot<RPW>(M + (long long)j0 * n, n, v, lane, p);
-      } else {
-        for (int q = 0; q < RPW; ++q) p[q] = 0.0;
-        for (int q = 0; q < jl; ++q) multi_dot<1>(M + (long long)(j0 + q) * n, n, v, lane, p + q);
-      }
+    double p[MC];
+    if (j < r1) {
+      part_dot<WPR, MC>(M + (long long)j * n, v, ldv, (int)n, warp % WPR, lane, p);
     } else {
 #pragma unroll
-      for (int q = 0; q < RPW; ++q) p[q] = 0.0;
+      for (int c = 0; c < MC; ++c) p[c] = 0.0;
     }
     if (lane == 0)
 #pragma unroll
-      for (int q = 0; q < RPW; ++q) red[warp * RPW + q] = p[q];
+      for (int c = 0; c < MC; ++c) red[c * kRedStride + warp] = p[c];
+  } else {
+    const int j0 = r0 + warp * RPW;
+    double p[RPW][MC];
+#pragma unroll
+    for (int q = 0; q < RPW; ++q)
+#pragma unroll
+      for (int c = 0; c < MC; ++c) p[q][c] = 0.0;
+    if (j0 < r1) {
+      const int jl = min(j0 + RPW, r1) - j0;
+      if (jl == RPW) {
+        multi_dot<RPW, MC>(M + (long long)j0 * n, n, v, ldv, lane, p);
+      } else {
+        for (int q = 0; q < jl; ++q) {
+          double t1[1][MC];
+          multi_dot<1, MC>(M + (long long)(j0 + q) * n, n, v, ldv, lane, t1);
+#pragma unroll
+          for (int c = 0; c < MC; ++c) p[q][c] = t1[0][c];
+        }
+      }
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < RPW; ++q)
+#pragma unroll
+        for (int c = 0; c < MC; ++c) red[c * kRedStride + warp * RPW + q] = p[q][c];
   }
   __syncthreads();
-  double d = 0.0;
-  if (threadIdx.x < kCoarseWarps * RPW / WPR) {
-    if (RPW == 1) {
 #pragma unroll
-      for (int k = 0; k < WPR; ++k) d += red[threadIdx.x * WPR + k];
-    } else {
-      d = red[threadIdx.x];
+  for (int c = 0; c < MC; ++c) d[c] = 0.0;
+  if (threadIdx.x < kCoarseWarps * RPW / WPR) {
+#pragma unroll
+    for (int c = 0; c < MC; ++c) {
+      if (RPW == 1) {
+#pragma unroll
+        for (int k = 0; k < WPR; ++k) d[c] += red[c * kRedStride + threadIdx.x * WPR + k];
+      } else {
+        d[c] = red[c * kRedStride + threadIdx.x];
+      }
     }
   }
-  return d;
 }
 
 // mode = WPR | RPW << 4 (RPW 0 or 1 = one row per warp)
@@ -149,24 +212,26 @@ __device__ __forceinline__ int mode_rows(int mode) {
   return kCoarseWarps * rpw / wpr;
 }
 
-__device__ __forceinline__ double rows_dot_w(int mode, const double* __restrict__ M, long long n, const double* v,
-                                             int r0, int r1, double* red) {
+template <int MC>
+__device__ __forceinline__ void rows_dot_w(int mode, const double* __restrict__ M, long long n, const double* v,
+                                           int ldv, int r0, int r1, double* red, double (&d)[MC]) {
   switch (mode) {
-    case 1: return rows_dot<1, 1>(M, n, v, r0, r1, red);
-    case 2: return rows_dot<2, 1>(M, n, v, r0, r1, red);
-    case 4: return rows_dot<4, 1>(M, n, v, r0, r1, red);
-    case 8: return rows_dot<8, 1>(M, n, v, r0, r1, red);
-    case 1 | (2 << 4): return rows_dot<1, 2>(M, n, v, r0, r1, red);
-    default: return rows_dot<1, 4>(M, n, v, r0, r1, red);
+    case 1: rows_dot<1, 1, MC>(M, n, v, ldv, r0, r1, red, d); break;
+    case 2: rows_dot<2, 1, MC>(M, n, v, ldv, r0, r1, red, d); break;
+    case 4: rows_dot<4, 1, MC>(M, n, v, ldv, r0, r1, red, d); break;
+    case 8: rows_dot<8, 1, MC>(M, n, v, ldv, r0, r1, red, d); break;
+    case 1 | (2 << 4): rows_dot<1, 2, MC>(M, n, v, ldv, r0, r1, red, d); break;
+    default: rows_dot<1, 4, MC>(M, n, v, ldv, r0, r1, red, d); break;
   }
 }
 
-// front position p of a node: base + child-0 entry + child-1 entry (fixed
-// order). cU is written during the solve: read through L2 (__ldcg).
-__device__ __forceinline__ double gather_front(const CoarseNDDev& D, long long gm, int p, double base) {
+// front position p of a node, column c: base + child-0 entry + child-1 entry
+// (fixed order). cU is written during the solve: read through L2 (__ldcg).
+__device__ __forceinline__ double gather_front(const CoarseNDDev& D, long long gm, int p, double base, int c) {
   const int g0 = __ldg(D.gmap + gm + 2 * p), g1 = __ldg(D.gmap + gm + 2 * p + 1);
-  if (g0 >= 0) base += __ldcg(D.cU + g0);
-  if (g1 >= 0) base += __ldcg(D.cU + g1);
+  const double* cu = D.cU + c * D.cu_ld;
+  if (g0 >= 0) base += __ldcg(cu + g0);
+  if (g1 >= 0) base += __ldcg(cu + g1);
   return base;
 }
 
@@ -196,9 +261,6 @@ __device__ __forceinline__ void fill_batched(double* dst, int n, F f) {
 
 // ---- item bodies (all threads of the CTA; contain __syncthreads) ----------
 
-// Forward rows: c_U[j] = f_U[j] - G[j,:] f_S. assembled: f_S / f_U were written
-// by the node's assembly item; else gathered here (the node's first item
-// also stores f_S for the backward pass).
 // A bottom node's layout (meta row: s, u, g_off, b_off, sd_off, ud_off, gm_off).
 struct NodeInfo {
   int s, u;
@@ -235,71 +297,110 @@ __device__ __forceinline__ NodeInfo item_record(const long long* __restrict__ re
   return n;
 }
 
+// Forward rows: c_U[j] = f_U[j] - G[j,:] f_S. assembled: f_S / f_U were written
+// by the node's assembly item; else gathered here (the node's first item
+// also stores f_S for the backward pass). fs: MC x s shared doubles.
+template <int MC>
 __device__ __forceinline__ void item_fwd(const CoarseNDDev& D, bool assembled, int wpr, const NodeInfo& n, int r0,
-                                         int r1, const double* y, double* fs, double* red) {
+                                         int r1, const ColSet& C, double* fs, double* red) {
   const int s = n.s;
   const long long g_off = n.g_off, sd_off = n.sd_off, ud_off = n.ud_off, gm = n.gm;
   if (assembled) {
-    fill_batched(fs, s, [&](int i) { return __ldcg(D.fS + sd_off + i); });
+    fill_batched(fs, MC * s, [&](int i) {
+      const int c = i / s, k = i - c * s;
+      return __ldcg(D.fS + c * D.fs_ld + sd_off + k);
+    });
   } else {
-    fill_batched(fs, s, [&](int i) { return gather_front(D, gm, i, y[sd_off + i]); });
+    fill_batched(fs, MC * s, [&](int i) {
+      const int c = i / s, k = i - c * s;
+      return gather_front(D, gm, k, C.y[c * C.ldy + sd_off + k], c);
+    });
     if (r0 == 0)
-      for (int i = threadIdx.x; i < s; i += blockDim.x) D.fS[sd_off + i] = fs[i];  // own writes: no barrier
+      for (int i = threadIdx.x; i < MC * s; i += blockDim.x) {  // own writes: no barrier
+        const int c = i / s, k = i - c * s;
+        D.fS[c * D.fs_ld + sd_off + k] = fs[i];
+      }
   }
   __syncthreads();
-  const double d = rows_dot_w(wpr, D.G + g_off, s, fs, r0, r1, red);
+  double d[MC];
+  rows_dot_w<MC>(wpr, D.G + g_off, s, fs, s, r0, r1, red, d);
   const int j = r0 + threadIdx.x;
   if (threadIdx.x < mode_rows(wpr) && j < r1) {
-    const double fu = assembled ? __ldcg(D.cU + ud_off + j) : gather_front(D, gm, s + j, 0.0);
-    D.cU[ud_off + j] = fu - d;
+#pragma unroll
+    for (int c = 0; c < MC; ++c) {
+      const double fu = assembled ? __ldcg(D.cU + c * D.cu_ld + ud_off + j) : gather_front(D, gm, s + j, 0.0, c);
+      D.cU[c * D.cu_ld + ud_off + j] = fu - d[c];
+    }
   }
 }
 
-// Large fronts, assembly: f_S -> fS, f_U -> cU (whole node).
-__device__ __forceinline__ void item_asm(const CoarseNDDev& D, const NodeInfo& n, const double* y) {
-  const int s = n.s, u = n.u;
+// Large fronts, assembly: f_S -> fS, f_U -> cU (whole node, all columns).
+template <int MC>
+__device__ __forceinline__ void item_asm(const CoarseNDDev& D, const NodeInfo& n, const ColSet& C) {
+  const int s = n.s, u = n.u, f = s + u;
   const long long sd_off = n.sd_off, ud_off = n.ud_off, gm = n.gm;
   batched(
-      s + u, [&](int p) { return gather_front(D, gm, p, p < s ? y[sd_off + p] : 0.0); },
-      [&](int p, double v) {
-        if (p < s) D.fS[sd_off + p] = v;
-        else D.cU[ud_off + p - s] = v;
+      MC * f,
+      [&](int i) {
+        const int c = i / f, p = i - c * f;
+        return gather_front(D, gm, p, p < s ? C.y[c * C.ldy + sd_off + p] : 0.0, c);
+      },
+      [&](int i, double v) {
+        const int c = i / f, p = i - c * f;
+        if (p < s) D.fS[c * D.fs_ld + sd_off + p] = v;
+        else D.cU[c * D.cu_ld + ud_off + p - s] = v;
       });
 }
 
-// Backward rows: x_S[j] = [Z | -G^T][j,:] . [f_S ; x_U].
-__device__ __forceinline__ void item_bwd(const CoarseNDDev& D, int wpr, const NodeInfo& n, int r0, int r1, double* x,
-                                         double* v, double* red) {
-  const int s = n.s, u = n.u;
+// Backward rows: x_S[j] = [Z | -G^T][j,:] . [f_S ; x_U]. v: MC x (s+u) shared.
+template <int MC>
+__device__ __forceinline__ void item_bwd(const CoarseNDDev& D, int wpr, const NodeInfo& n, int r0, int r1,
+                                         const ColSet& C, double* v, double* red) {
+  const int s = n.s, u = n.u, f = s + u;
   const long long b_off = n.b_off, sd_off = n.sd_off, ud_off = n.ud_off;
-  fill_batched(v, s + u, [&](int i) {
-    return i < s ? __ldcg(D.fS + sd_off + i) : __ldcg(x + __ldg(D.udof + ud_off + i - s));
+  fill_batched(v, MC * f, [&](int i) {
+    const int c = i / f, k = i - c * f;
+    return k < s ? __ldcg(D.fS + c * D.fs_ld + sd_off + k) : __ldcg(C.x + c * C.ldx + __ldg(D.udof + ud_off + k - s));
   });
   __syncthreads();
-  const double d = rows_dot_w(wpr, D.B + b_off, s + u, v, r0, r1, red);
+  double d[MC];
+  rows_dot_w<MC>(wpr, D.B + b_off, f, v, f, r0, r1, red, d);
   const int j = r0 + threadIdx.x;
-  if (threadIdx.x < mode_rows(wpr) && j < r1) x[sd_off + j] = d;
+  if (threadIdx.x < mode_rows(wpr) && j < r1)
+#pragma unroll
+    for (int c = 0; c < MC; ++c) C.x[c * C.ldx + sd_off + j] = d[c];
 }
 
 // Top set, gather: fT[i] = y_T[i] + children's update entries (CSR, fixed order).
-__device__ __forceinline__ void item_top_gather(const CoarseNDDev& D, int i0, int i1, const double* y) {
+template <int MC>
+__device__ __forceinline__ void item_top_gather(const CoarseNDDev& D, int i0, int i1, const ColSet& C) {
   const int i = i0 + threadIdx.x;
   if (i >= i1) return;
-  double v = y[D.top_off + i];
   const int a = __ldg(D.tptr + i), b = __ldg(D.tptr + i + 1);
-  for (int k = a; k < b; ++k) v += __ldcg(D.cU + __ldg(D.tidx + k));
-  D.fT[i] = v;
+#pragma unroll
+  for (int c = 0; c < MC; ++c) {
+    double v = C.y[c * C.ldy + D.top_off + i];
+    for (int k = a; k < b; ++k) v += __ldcg(D.cU + c * D.cu_ld + __ldg(D.tidx + k));
+    D.fT[c * D.ft_ld + i] = v;
+  }
 }
 
-// Top set, rows: x_T = S_T^-1 fT.
-__device__ __forceinline__ void item_top_rows(const CoarseNDDev& D, int wpr, int r0, int r1, double* x, double* ft,
-                                              double* red) {
+// Top set, rows: x_T = S_T^-1 fT. ft: MC x n_top shared.
+template <int MC>
+__device__ __forceinline__ void item_top_rows(const CoarseNDDev& D, int wpr, int r0, int r1, const ColSet& C,
+                                              double* ft, double* red) {
   const int n = D.n_top;
-  fill_batched(ft, n, [&](int i) { return __ldcg(D.fT + i); });
+  fill_batched(ft, MC * n, [&](int i) {
+    const int c = i / n, k = i - c * n;
+    return __ldcg(D.fT + c * D.ft_ld + k);
+  });
   __syncthreads();
-  const double d = rows_dot_w(wpr, D.ZT, n, ft, r0, r1, red);
+  double d[MC];
+  rows_dot_w<MC>(wpr, D.ZT, n, ft, n, r0, r1, red, d);
   const int j = r0 + threadIdx.x;
-  if (threadIdx.x < mode_rows(wpr) && j < r1) x[D.top_off + j] = d;
+  if (threadIdx.x < mode_rows(wpr) && j < r1)
+#pragma unroll
+    for (int c = 0; c < MC; ++c) C.x[c * C.ldx + D.top_off + j] = d[c];
 }
 
 // ---- persistent dataflow schedule -------------------------------------------
@@ -311,12 +412,12 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 
 // item record (12 ints): type, wpr, node, r0, r1, wait_idx, wait_need,
 // done_idx, done_need, rel_begin, rel_end, 0
-__global__ void __launch_bounds__(kCoarseThreads) k_coarse_flow(CoarseNDDev D, const double* y, double* x,
-                                                                const int* stop) {
+template <int MC>
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_flow(CoarseNDDev D, ColSet C) {
   extern __shared__ double sm[];
-  __shared__ double red[4 * kCoarseWarps];
+  __shared__ double red[MC * kRedStride];
   __shared__ int s_item;
-  if (stop != nullptr && *stop) return;
+  if (all_stopped<MC>(C)) return;
   const unsigned long long E = __ldcg(D.ctl + 2) + 1;  // this solve's epoch (1-based)
   unsigned long long* cnt = D.cnt;
   while (true) {
@@ -343,12 +444,12 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_flow(CoarseNDDev D, c
     }
     __syncthreads();
     switch (type) {
-      case kFwd: item_fwd(D, false, wpr, node_info(D.meta + 8 * node), r0, r1, y, sm, red); break;
-      case kAsm: item_asm(D, node_info(D.meta + 8 * node), y); break;
-      case kRows: item_fwd(D, true, wpr, node_info(D.meta + 8 * node), r0, r1, y, sm, red); break;
-      case kTopGather: item_top_gather(D, r0, r1, y); break;
-      case kTopRows: item_top_rows(D, wpr, r0, r1, x, sm, red); break;
-      default: item_bwd(D, wpr, node_info(D.meta + 8 * node), r0, r1, x, sm, red); break;
+      case kFwd: item_fwd<MC>(D, false, wpr, node_info(D.meta + 8 * node), r0, r1, C, sm, red); break;
+      case kAsm: item_asm<MC>(D, node_info(D.meta + 8 * node), C); break;
+      case kRows: item_fwd<MC>(D, true, wpr, node_info(D.meta + 8 * node), r0, r1, C, sm, red); break;
+      case kTopGather: item_top_gather<MC>(D, r0, r1, C); break;
+      case kTopRows: item_top_rows<MC>(D, wpr, r0, r1, C, sm, red); break;
+      default: item_bwd<MC>(D, wpr, node_info(D.meta + 8 * node), r0, r1, C, sm, red); break;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -373,45 +474,48 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_flow(CoarseNDDev D, c
 }
 
 // ---- per-level schedule (fallback) -----------------------------------------
+template <int MC>
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_fwd(CoarseNDDev D, int wpr, int assembled,
-                                                               const long long* recs, const double* y,
-                                                               const int* stop) {
+                                                               const long long* recs, ColSet C) {
   extern __shared__ double sm[];
-  __shared__ double red[4 * kCoarseWarps];
-  if (stop != nullptr && *stop) return;
+  __shared__ double red[MC * kRedStride];
+  if (all_stopped<MC>(C)) return;
   int r0, r1;
   const NodeInfo n = item_record(recs + 10LL * blockIdx.x, r0, r1);
-  item_fwd(D, assembled != 0, wpr, n, r0, r1, y, sm, red);
+  item_fwd<MC>(D, assembled != 0, wpr, n, r0, r1, C, sm, red);
 }
 
-__global__ void __launch_bounds__(kCoarseThreads) k_coarse_asm(CoarseNDDev D, const int* nodes, const double* y,
-                                                               const int* stop) {
-  if (stop != nullptr && *stop) return;
-  item_asm(D, node_info(D.meta + 8 * nodes[blockIdx.x]), y);
+template <int MC>
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_asm(CoarseNDDev D, const int* nodes, ColSet C) {
+  if (all_stopped<MC>(C)) return;
+  item_asm<MC>(D, node_info(D.meta + 8 * nodes[blockIdx.x]), C);
 }
 
+template <int MC>
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_bwd(CoarseNDDev D, int wpr, const long long* recs,
-                                                               double* x, const int* stop) {
+                                                               ColSet C) {
   extern __shared__ double sm[];
-  __shared__ double red[4 * kCoarseWarps];
-  if (stop != nullptr && *stop) return;
+  __shared__ double red[MC * kRedStride];
+  if (all_stopped<MC>(C)) return;
   int r0, r1;
   const NodeInfo n = item_record(recs + 10LL * blockIdx.x, r0, r1);
-  item_bwd(D, wpr, n, r0, r1, x, sm, red);
+  item_bwd<MC>(D, wpr, n, r0, r1, C, sm, red);
 }
 
-__global__ void k_coarse_top_gather(CoarseNDDev D, const double* y, const int* stop) {
-  if (stop != nullptr && *stop) return;
-  item_top_gather(D, blockIdx.x * blockDim.x, D.n_top, y);
+template <int MC>
+__global__ void k_coarse_top_gather(CoarseNDDev D, ColSet C) {
+  if (all_stopped<MC>(C)) return;
+  item_top_gather<MC>(D, blockIdx.x * blockDim.x, D.n_top, C);
 }
 
-__global__ void __launch_bounds__(kCoarseThreads) k_coarse_top_rows(CoarseNDDev D, double* x, const int* stop) {
+template <int MC>
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_top_rows(CoarseNDDev D, ColSet C) {
   extern __shared__ double sm[];
-  __shared__ double red[4 * kCoarseWarps];
-  if (stop != nullptr && *stop) return;
+  __shared__ double red[MC * kRedStride];
+  if (all_stopped<MC>(C)) return;
   const int rpc = mode_rows(D.top_wpr);
   const int r0 = blockIdx.x * rpc;
-  item_top_rows(D, D.top_wpr, r0, min(D.n_top, r0 + rpc), x, sm, red);
+  item_top_rows<MC>(D, D.top_wpr, r0, min(D.n_top, r0 + rpc), C, sm, red);
 }
 
 template <typename K>
@@ -419,17 +523,36 @@ static void allow_smem(K kernel, int bytes) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-cudaError_t launch_coarse_nd(const CoarseNDDev& D, const double* y, double* x, const int* stop, cudaStream_t s) {
-  static int attr_max = 0;
+static int max_optin_smem() {
+  static int v = 0;
+  if (v == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (v <= 0) v = 227 * 1024;
+  }
+  return v;
+}
+
+// per-column shared footprint of the row items (front / separator / top vectors)
+static int col_smem(const CoarseNDDev& D) {
   const int smem_bwd = (int)(sizeof(double) * (size_t)D.max_front);
-  const int smem_fwd = (int)(sizeof(double) * (size_t)D.max_sep);
   const int smem_top = (int)(sizeof(double) * (size_t)(D.n_top + 1));
-  const int smem_max = std::max(smem_bwd, smem_top);
+  return std::max(smem_bwd, smem_top);
+}
+
+template <int MC>
+static cudaError_t launch_coarse_cols(const CoarseNDDev& D, const ColSet& C, cudaStream_t s) {
+  static int attr_max = 0;
+  const int smem_fwd = MC * (int)(sizeof(double) * (size_t)D.max_sep);
+  const int smem_bwd = MC * (int)(sizeof(double) * (size_t)D.max_front);
+  const int smem_top = MC * (int)(sizeof(double) * (size_t)(D.n_top + 1));
+  const int smem_max = MC * col_smem(D);
   if (smem_max > attr_max) {
-    allow_smem(k_coarse_flow, smem_max);
-    allow_smem(k_coarse_fwd, smem_max);
-    allow_smem(k_coarse_bwd, smem_max);
-    allow_smem(k_coarse_top_rows, smem_max);
+    allow_smem(k_coarse_flow<MC>, smem_max);
+    allow_smem(k_coarse_fwd<MC>, smem_max);
+    allow_smem(k_coarse_bwd<MC>, smem_max);
+    allow_smem(k_coarse_top_rows<MC>, smem_max);
     attr_max = smem_max;
   }
   if (D.items != nullptr && D.n_items > 0) {
@@ -438,12 +561,12 @@ cudaError_t launch_coarse_nd(const CoarseNDDev& D, const double* y, double* x, c
       int dev = 0, nsm = 148, per_sm = 1;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_flow, kCoarseThreads, smem_max);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_flow<MC>, kCoarseThreads, smem_max);
       cached_ctas = nsm * std::max(1, per_sm);
       cached_smem = smem_max;
     }
     const int ctas = std::min(cached_ctas, D.n_items);
-    k_coarse_flow<<<(unsigned)ctas, kCoarseThreads, smem_max, s>>>(D, y, x, stop);
+    k_coarse_flow<MC><<<(unsigned)ctas, kCoarseThreads, smem_max, s>>>(D, C);
     return cudaGetLastError();
   }
   for (int h = 0; h < D.n_levels; ++h) {
@@ -452,22 +575,51 @@ cudaError_t launch_coarse_nd(const CoarseNDDev& D, const double* y, double* x, c
     const int split = D.split[h] != 0;
     if (split) {
       const long long na = D.asm_ptr[h], nb = D.asm_ptr[h + 1];
-      k_coarse_asm<<<(unsigned)(nb - na), kCoarseThreads, 0, s>>>(D, D.asm_nodes + na, y, stop);
+      k_coarse_asm<MC><<<(unsigned)(nb - na), kCoarseThreads, 0, s>>>(D, D.asm_nodes + na, C);
     }
-    k_coarse_fwd<<<(unsigned)(b - a), kCoarseThreads, smem_fwd, s>>>(D, D.fwd_wpr[h], split, D.fwd_items + 10 * a, y,
-                                                                      stop);
+    k_coarse_fwd<MC><<<(unsigned)(b - a), kCoarseThreads, smem_fwd, s>>>(D, D.fwd_wpr[h], split,
+                                                                         D.fwd_items + 10 * a, C);
   }
   if (D.n_top > 0) {
-    k_coarse_top_gather<<<(unsigned)((D.n_top + 255) / 256), 256, 0, s>>>(D, y, stop);
+    k_coarse_top_gather<MC><<<(unsigned)((D.n_top + 255) / 256), 256, 0, s>>>(D, C);
     const int rpc = kCoarseWarps * std::max(1, D.top_wpr >> 4) / (D.top_wpr & 15);
-    k_coarse_top_rows<<<(unsigned)((D.n_top + rpc - 1) / rpc), kCoarseThreads, smem_top, s>>>(D, x, stop);
+    k_coarse_top_rows<MC><<<(unsigned)((D.n_top + rpc - 1) / rpc), kCoarseThreads, smem_top, s>>>(D, C);
   }
   for (int h = 0; h < D.n_levels; ++h) {  // bwd groups: top-most bottom level first
     const long long a = D.bwd_ptr[h], b = D.bwd_ptr[h + 1];
     if (b > a)
-      k_coarse_bwd<<<(unsigned)(b - a), kCoarseThreads, smem_bwd, s>>>(D, D.bwd_wpr[h], D.bwd_items + 10 * a, x, stop);
+      k_coarse_bwd<MC><<<(unsigned)(b - a), kCoarseThreads, smem_bwd, s>>>(D, D.bwd_wpr[h], D.bwd_items + 10 * a, C);
   }
   return cudaGetLastError();
+}
+
+int coarse_nd_max_cols(const CoarseNDDev& D) {
+  const int per = std::max(col_smem(D), 8);
+  return std::max(1, std::min({kCoarseMaxCols, D.max_cols > 0 ? D.max_cols : 1, max_optin_smem() / per}));
+}
+
+cudaError_t launch_coarse_nd_multi(const CoarseNDDev& D, int ncols, const double* y, long long ldy, double* x,
+                                   long long ldx, const int* stop, long long stop_ld, cudaStream_t s) {
+  const int mc = coarse_nd_max_cols(D);
+  // column groups of <= mc run one after another in stream order and share
+  // the per-column scratch (fS / cU / fT columns 0 .. mc-1)
+  for (int c0 = 0; c0 < ncols; c0 += mc) {
+    const int k = std::min(mc, ncols - c0);
+    ColSet C{y + c0 * ldy, ldy, x + c0 * ldx, ldx, stop ? stop + c0 * stop_ld : nullptr, stop_ld};
+    cudaError_t e;
+    switch (k) {
+      case 1: e = launch_coarse_cols<1>(D, C, s); break;
+      case 2: e = launch_coarse_cols<2>(D, C, s); break;
+      case 3: e = launch_coarse_cols<3>(D, C, s); break;
+      default: e = launch_coarse_cols<4>(D, C, s); break;
+    }
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_coarse_nd(const CoarseNDDev& D, const double* y, double* x, const int* stop, cudaStream_t s) {
+  return launch_coarse_nd_multi(D, 1, y, 0, x, 0, stop, 0, s);
 }
 
 }  // namespace tvb

@@ -40,8 +40,20 @@ struct CoarseNDDev {
   const int* rel;             // counters released by a node's last finishing item
   unsigned long long* cnt;    // dependency counters (epoch-scaled, never reset)
   unsigned long long* ctl;    // [3]: next item, CTAs exited, epoch
+  // multi-RHS scratch: column c of fS / cU / fT at + c * fs_ld / cu_ld / ft_ld
+  long long fs_ld, cu_ld, ft_ld;
+  int max_cols;               // scratch columns allocated (>= 1)
 };
 
+constexpr int kCoarseMaxCols = 4;  // right-hand sides per coarse-solve launch
+
 cudaError_t launch_coarse_nd(const CoarseNDDev& D, const double* y, double* x, const int* stop, cudaStream_t s);
+// ncols right-hand sides (column c of y / x at + c * ldy / ldx); column c is
+// skipped work-wise only when every column of its launch group is stopped
+// (stop[c * stop_ld] != 0). Per-column results are bitwise those of
+// launch_coarse_nd on that column alone.
+cudaError_t launch_coarse_nd_multi(const CoarseNDDev& D, int ncols, const double* y, long long ldy, double* x,
+                                   long long ldx, const int* stop, long long stop_ld, cudaStream_t s);
+int coarse_nd_max_cols(const CoarseNDDev& D);
 
 }  // namespace tvb

@@ -32,23 +32,58 @@
 namespace tvb {
 
 // mu = Einv * yc with a dense symmetric inverse; one warp per row, fixed order.
-__global__ void k_dense_gemv(long long nc, const double* Einv, const double* yc, double* mu, const int* stop) {
-  if (stop != nullptr && *stop) return;
+// MC right-hand sides share each row load; per column the arithmetic is the
+// single-column sequence (bitwise equal results).
+template <int MC>
+__global__ void k_dense_gemv(long long nc, const double* Einv, const double* yc, long long ldy, double* mu,
+                            long long ldm, const int* stop, long long stop_ld) {
+  if (stop != nullptr) {
+    bool all = true;
+#pragma unroll
+    for (int c = 0; c < MC; ++c) all = all && stop[c * stop_ld] != 0;
+    if (all) return;
+  }
   const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= nc) return;
   const double* a = Einv + row * nc;
-  double s = 0.0;
-  for (long long j = lane; j < nc; j += 32) s = fma(a[j], yc[j], s);
-  s = warp_sum(s);
-  if (lane == 0) mu[row] = s;
+  double s[MC];
+#pragma unroll
+  for (int c = 0; c < MC; ++c) s[c] = 0.0;
+  for (long long j = lane; j < nc; j += 32) {
+    const double aj = a[j];
+#pragma unroll
+    for (int c = 0; c < MC; ++c) s[c] = fma(aj, yc[c * ldy + j], s[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < MC; ++c) {
+    const double v = warp_sum(s[c]);
+    if (lane == 0) mu[c * ldm + row] = v;
+  }
+}
+
+cudaError_t launch_dense_gemv_multi(long long nc, const double* Einv, int ncols, const double* yc, long long ldy,
+                                    double* mu, long long ldm, const int* stop, long long stop_ld, cudaStream_t s) {
+  const long long threads = nc * 32;
+  const unsigned grid = (unsigned)((threads + 255) / 256);
+  for (int c0 = 0; c0 < ncols; c0 += 4) {
+    const int k = ncols - c0 < 4 ? ncols - c0 : 4;
+    const double* y = yc + c0 * ldy;
+    double* m = mu + c0 * ldm;
+    const int* st = stop ? stop + c0 * stop_ld : nullptr;
+    switch (k) {
+      case 1: k_dense_gemv<1><<<grid, 256, 0, s>>>(nc, Einv, y, ldy, m, ldm, st, stop_ld); break;
+      case 2: k_dense_gemv<2><<<grid, 256, 0, s>>>(nc, Einv, y, ldy, m, ldm, st, stop_ld); break;
+      case 3: k_dense_gemv<3><<<grid, 256, 0, s>>>(nc, Einv, y, ldy, m, ldm, st, stop_ld); break;
+      default: k_dense_gemv<4><<<grid, 256, 0, s>>>(nc, Einv, y, ldy, m, ldm, st, stop_ld); break;
+    }
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_dense_gemv(long long nc, const double* Einv, const double* yc, double* mu, const int* stop,
                               cudaStream_t s) {
-  const long long threads = nc * 32;
-  k_dense_gemv<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(nc, Einv, yc, mu, stop);
-  return cudaGetLastError();
+  return launch_dense_gemv_multi(nc, Einv, 1, yc, 0, mu, 0, stop, 0, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -110,19 +145,40 @@ static PcgWork carve(void* ws, const Grid& g, int block) {
     }                                                \
   } while (0)
 
-int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
+// m = P.nrhs independent right-hand sides against one operator / coarse
+// factor (multi-RHS batching). Each RHS owns a complete
+// single-solve workspace (RHS c at ws + c * per, so its coarse vectors sit at a
+// fixed stride from RHS 0's and one coarse-solve launch serves all of them);
+// every RHS runs the single-RHS kernels on its own vectors and state and stops
+// on its own criterion, so its iterates, iteration count and result are
+// bitwise those of solving it alone. Shared per iteration: the coarse solve
+// (one pass over the factor for all RHS) and the graph launch / host check.
+int pcg_solve_multi(const PcgProblem& P, PcgResult* R, int* rstat, cudaStream_t user_stream) {
   const Grid& G = P.g;
   const long long nd = 3 * G.nn;
+  const int m = P.nrhs;
+  if (m < 1 || m > kPcgMaxRhs) {
+    set_last_error("number of right-hand sides out of range");
+    return kStatusBadArg;
+  }
   const bool defl = P.block > 0 && (P.coarse_kind == 1 || P.coarse != nullptr);
   Agglo A{};
   if (defl) A = make_agglo(G, P.block, P.h);
-  if (P.ws_bytes < pcg_ws_bytes(G, defl ? P.block : 0)) {
+  const size_t per = pcg_ws_bytes(G, defl ? P.block : 0);
+  if (P.ws_bytes < per * (size_t)m) {
     set_last_error("pcg workspace too small");
     return kStatusWorkspace;
   }
-  PcgWork W = carve(P.ws, G, defl ? P.block : 0);
+  PcgWork W[kPcgMaxRhs];
+  for (int c = 0; c < m; ++c) W[c] = carve((char*)P.ws + per * c, G, defl ? P.block : 0);
+  const long long ldc = (long long)(per / sizeof(double));  // coarse-vector stride between RHS
+  const long long ld_done = (long long)(per / sizeof(int));  // SolverState::done stride between RHS
   DeflData D{const_cast<double*>(P.cen), const_cast<double*>(P.S), const_cast<int*>(P.keep)};
   if (P.coarse_kind == 1) D.perm = P.nd.perm;  // coarse vectors in the factor's ND order
+  for (int c = 0; c < m; ++c) {
+    R[c] = PcgResult{};
+    rstat[c] = kStatusOk;
+  }
 
   int dev = 0;
   TVB_CK(cudaGetDevice(&dev));
@@ -143,7 +199,7 @@ int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
     ~StreamGuard() { cudaStreamDestroy(s); }
   } guard{s};
 
-  auto matvec = [&](const double* u, double* y, bool with_dot, const int* stop) {
+  auto matvec = [&](int c, const double* u, double* y, bool with_dot, const int* stop) {
     MatvecParams mp{};
     mp.g = G;
     mp.u = u;
@@ -153,18 +209,22 @@ int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
     mp.mask_in = 0;  // solver vectors are already zero on fixed DOFs
     mp.mask_out = 1;
     mp.accumulate = 0;
-    mp.dot_partial = with_dot ? W.partials + 2 * kMaxReduceCtas : nullptr;
+    mp.dot_partial = with_dot ? W[c].partials + 2 * kMaxReduceCtas : nullptr;
     mp.stop = stop;
     return launch_matvec(plan, mp, P.modal, s);
   };
-  auto coarse_project = [&](const double* v, const int* stop, const double* v2 = nullptr) -> cudaError_t {
-    // nu = S E^-1 W^T (v + beta v2)  (v = f, A z ; v2 = q)
-    cudaError_t e = launch_restrict(A, P.nflags, D, v, W.yc, s, stop, v2, W.st);
+  // mu = E^-1 yc for RHS [c0, c0 + k) (one pass over the coarse factor)
+  auto coarse_solve = [&](int c0, int k, const int* stop) -> cudaError_t {
+    const int* st = stop ? &W[c0].st->done : nullptr;
+    if (P.coarse_kind == 1) return launch_coarse_nd_multi(P.nd, k, W[c0].yc, ldc, W[c0].mu, ldc, st, ld_done, s);
+    return launch_dense_gemv_multi(6 * A.nb, P.coarse, k, W[c0].yc, ldc, W[c0].mu, ldc, st, ld_done, s);
+  };
+  auto coarse_project = [&](int c, const double* v) -> cudaError_t {
+    // nu = S E^-1 W^T v  (prologue: v = f or A z)
+    cudaError_t e = launch_restrict(A, P.nflags, D, v, W[c].yc, s, nullptr, nullptr, W[c].st);
     if (e != cudaSuccess) return e;
-    if (P.coarse_kind == 1) e = launch_coarse_nd(P.nd, W.yc, W.mu, stop, s);
-    else e = launch_dense_gemv(6 * A.nb, P.coarse, W.yc, W.mu, stop, s);
-    if (e != cudaSuccess) return e;
-    return launch_block_nu(A, D, W.mu, W.nu, s, stop);
+    if ((e = coarse_solve(c, 1, nullptr)) != cudaSuccess) return e;
+    return launch_block_nu(A, D, W[c].mu, W[c].nu, s, nullptr);
   };
 
   // Optional (TVB_L2_PERSIST=1): keep the nested-dissection coarse factor
@@ -189,61 +249,83 @@ int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
     cudaGetLastError();  // the window is an optimisation only
   }
 
-  // --- prologue ------------------------------------------------------------
-  SolverState st0{};
-  st0.tol = P.tol;
-  st0.max_iters = P.max_iters;
-  TVB_CK(cudaMemcpyAsync(W.st, &st0, sizeof(st0), cudaMemcpyHostToDevice, s));
-  TVB_CK(cudaMemsetAsync(W.zero_free, 0, sizeof(int), s));
-  TVB_CK(launch_free_norm(nd, P.f, P.nflags, W.partials, W.st, s));
-  TVB_CK(launch_inv_diag(G, P.occ, P.nflags, P.kdiag, W.inv_d, nullptr, W.zero_free, s));
-  SolverState hst{};
+  // --- prologue (per RHS) ----------------------------------------------------
+  // The Jacobi diagonal depends on the operator only: built once (RHS 0's
+  // workspace) and read by every RHS.
+  const double* inv_d = W[0].inv_d;
+  TVB_CK(cudaMemsetAsync(W[0].zero_free, 0, sizeof(int), s));
+  TVB_CK(launch_inv_diag(G, P.occ, P.nflags, P.kdiag, W[0].inv_d, nullptr, W[0].zero_free, s));
   int zero_free = 0;
-  TVB_CK(cudaMemcpyAsync(&hst, W.st, sizeof(hst), cudaMemcpyDeviceToHost, s));
-  TVB_CK(cudaMemcpyAsync(&zero_free, W.zero_free, sizeof(int), cudaMemcpyDeviceToHost, s));
-  TVB_CK(cudaStreamSynchronize(s));
-  R.fnorm = hst.fnorm;
-  if (hst.fnorm == 0.0) {
-    TVB_CK(cudaMemsetAsync(P.x, 0, nd * sizeof(double), s));
+  TVB_CK(cudaMemcpyAsync(&zero_free, W[0].zero_free, sizeof(int), cudaMemcpyDeviceToHost, s));
+  bool active[kPcgMaxRhs];
+  int n_active = 0;
+  const int one = 1;
+  for (int c = 0; c < m; ++c) {
+    active[c] = false;
+    SolverState st0{};
+    st0.tol = P.tol;
+    st0.max_iters = P.max_iters;
+    TVB_CK(cudaMemcpyAsync(W[c].st, &st0, sizeof(st0), cudaMemcpyHostToDevice, s));
+    TVB_CK(launch_free_norm(nd, P.fs[c], P.nflags, W[c].partials, W[c].st, s));
+    SolverState hst{};
+    TVB_CK(cudaMemcpyAsync(&hst, W[c].st, sizeof(hst), cudaMemcpyDeviceToHost, s));
     TVB_CK(cudaStreamSynchronize(s));
-    R.iterations = 0;
-    R.residual = 0.0;
+    R[c].fnorm = hst.fnorm;
+    if (hst.fnorm == 0.0) {  // zero load: zero solution in 0 iterations (fea.py:243-245)
+      TVB_CK(cudaMemsetAsync(P.xs[c], 0, nd * sizeof(double), s));
+      TVB_CK(cudaMemcpyAsync(&W[c].st->done, &one, sizeof(int), cudaMemcpyHostToDevice, s));
+      TVB_CK(cudaStreamSynchronize(s));
+      continue;
+    }
+    if (zero_free > 0) {
+      set_last_error("zero stiffness diagonal on a loaded free DOF");
+      rstat[c] = kStatusSingular;
+      TVB_CK(cudaMemcpyAsync(&W[c].st->done, &one, sizeof(int), cudaMemcpyHostToDevice, s));
+      TVB_CK(cudaStreamSynchronize(s));
+      continue;
+    }
+    double* x = P.xs[c];
+    // x0
+    if (defl) {
+      TVB_CK(coarse_project(c, P.fs[c]));
+      TVB_CK(launch_prolong(A, P.nflags, D, W[c].nu, x, nullptr, nullptr, 0, s));
+    } else {
+      TVB_CK(cudaMemsetAsync(x, 0, nd * sizeof(double), s));
+    }
+    // r = f - A x0 ; z = D^-1 r ; rz ; res
+    TVB_CK(matvec(c, x, W[c].r, false, nullptr));
+    TVB_CK(launch_pcg_init(nd, P.fs[c], W[c].r, W[c].z, inv_d, P.nflags, 1, W[c].partials, W[c].st, s));
+    TVB_CK(cudaMemcpyAsync(&hst, W[c].st, sizeof(hst), cudaMemcpyDeviceToHost, s));
+    TVB_CK(cudaStreamSynchronize(s));
+    if (hst.done) {
+      TVB_CK(launch_zero_fixed(G.nn, x, P.nflags, s));
+      TVB_CK(cudaStreamSynchronize(s));
+      R[c].residual = hst.res;
+      continue;
+    }
+    // p = z - W E^-1 W^T A z  (or p = z)
+    if (defl) {
+      TVB_CK(matvec(c, W[c].z, W[c].q, false, nullptr));
+      TVB_CK(coarse_project(c, W[c].q));
+      TVB_CK(launch_prolong(A, P.nflags, D, W[c].nu, W[c].p, W[c].z, W[c].st, 2, s));
+    } else {
+      TVB_CK(cudaMemcpyAsync(W[c].p, W[c].z, nd * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+    active[c] = true;
+    ++n_active;
+  }
+  if (n_active == 0) {
+    for (int c = 0; c < m; ++c)
+      if (rstat[c] != kStatusOk) return rstat[c];
     return kStatusOk;
   }
-  if (zero_free > 0) {
-    set_last_error("zero stiffness diagonal on a loaded free DOF");
-    return kStatusSingular;
-  }
-  // x0
-  if (defl) {
-    TVB_CK(coarse_project(P.f, nullptr));
-    TVB_CK(launch_prolong(A, P.nflags, D, W.nu, P.x, nullptr, nullptr, 0, s));
-  } else {
-    TVB_CK(cudaMemsetAsync(P.x, 0, nd * sizeof(double), s));
-  }
-  // r = f - A x0 ; z = D^-1 r ; rz ; res
-  TVB_CK(matvec(P.x, W.r, false, nullptr));
-  TVB_CK(launch_pcg_init(nd, P.f, W.r, W.z, W.inv_d, P.nflags, 1, W.partials, W.st, s));
-  TVB_CK(cudaMemcpyAsync(&hst, W.st, sizeof(hst), cudaMemcpyDeviceToHost, s));
-  TVB_CK(cudaStreamSynchronize(s));
-  if (hst.done) {
-    TVB_CK(launch_zero_fixed(G.nn, P.x, P.nflags, s));
-    TVB_CK(cudaStreamSynchronize(s));
-    R.iterations = 0;
-    R.residual = hst.res;
-    return kStatusOk;
-  }
-  // p = z - W E^-1 W^T A z  (or p = z)
-  if (defl) {
-    TVB_CK(matvec(W.z, W.q, false, nullptr));
-    TVB_CK(coarse_project(W.q, nullptr));
-    TVB_CK(launch_prolong(A, P.nflags, D, W.nu, W.p, W.z, W.st, 2, s));
-  } else {
-    TVB_CK(cudaMemcpyAsync(W.p, W.z, nd * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  }
+  // RHS that stopped in the prologue are inert in the graph (done flag set);
+  // the coarse solve runs over the contiguous range of RHS that can be active
+  int c_lo = 0, c_hi = m;
+  while (!active[c_lo]) ++c_lo;
+  while (!active[c_hi - 1]) --c_hi;
 
   // --- iteration graph -----------------------------------------------------
-  const int* stop = &W.st->done;
   // TVB_SOLVE_SKIP (timing experiments only -- the iterates are then wrong):
   // bitmask of iteration stages left out of the graph, 1 A p, 2 update, 4 A z,
   // 8 restriction, 16 coarse solve, 32 nu + prolongation; the in-graph cost of
@@ -251,54 +333,62 @@ int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
   const int skip = getenv("TVB_SOLVE_SKIP") ? atoi(getenv("TVB_SOLVE_SKIP")) : 0;
   auto one_iteration = [&]() -> cudaError_t {
     cudaError_t e = cudaSuccess;
-    if (!(skip & 1) && (e = matvec(W.p, W.q, true, stop)) != cudaSuccess) return e;
-    if (!(skip & 2) &&
-        (e = launch_pcg_update(nd, defl ? nullptr : P.x, W.r, W.z, W.p, W.q, W.inv_d, W.st, W.partials,
-                               W.partials + 2 * kMaxReduceCtas, plan.nblocks(), s)) != cudaSuccess)
-      return e;
-    if (defl) {
-      if (!(skip & 4) && (e = matvec(W.z, W.t, false, stop)) != cudaSuccess) return e;
-      if (!(skip & 8) && (e = launch_restrict(A, P.nflags, D, W.t, W.yc, s, stop, W.q, W.st)) != cudaSuccess)
+    for (int c = c_lo; c < c_hi; ++c) {
+      const int* stop = &W[c].st->done;
+      if (!(skip & 1) && (e = matvec(c, W[c].p, W[c].q, true, stop)) != cudaSuccess) return e;
+      if (!(skip & 2) &&
+          (e = launch_pcg_update(nd, defl ? nullptr : P.xs[c], W[c].r, W[c].z, W[c].p, W[c].q, inv_d, W[c].st,
+                                 W[c].partials, W[c].partials + 2 * kMaxReduceCtas, plan.nblocks(), s)) !=
+              cudaSuccess)
         return e;
-      if (!(skip & 16)) {
-        e = P.coarse_kind == 1 ? launch_coarse_nd(P.nd, W.yc, W.mu, stop, s)
-                               : launch_dense_gemv(6 * A.nb, P.coarse, W.yc, W.mu, stop, s);
-        if (e != cudaSuccess) return e;
+      if (!defl) {
+        if ((e = launch_pcg_pupdate(nd, W[c].p, W[c].z, W[c].st, s)) != cudaSuccess) return e;
+        continue;
       }
-      if (skip & 32) return cudaSuccess;
-      if ((e = launch_block_nu(A, D, W.mu, W.nu, s, stop)) != cudaSuccess) return e;
-      // p = z + beta p - W nu, and the deferred x += alpha p_old of this iteration
-      return launch_prolong(A, P.nflags, D, W.nu, W.p, W.z, W.st, 1, s, P.x);
+      if (!(skip & 4) && (e = matvec(c, W[c].z, W[c].t, false, stop)) != cudaSuccess) return e;
+      if (!(skip & 8) &&
+          (e = launch_restrict(A, P.nflags, D, W[c].t, W[c].yc, s, stop, W[c].q, W[c].st)) != cudaSuccess)
+        return e;
     }
-    return launch_pcg_pupdate(nd, W.p, W.z, W.st, s);
+    if (!defl) return cudaSuccess;
+    if (!(skip & 16) && (e = coarse_solve(c_lo, c_hi - c_lo, &W[c_lo].st->done)) != cudaSuccess) return e;
+    if (skip & 32) return cudaSuccess;
+    for (int c = c_lo; c < c_hi; ++c) {
+      const int* stop = &W[c].st->done;
+      if ((e = launch_block_nu(A, D, W[c].mu, W[c].nu, s, stop)) != cudaSuccess) return e;
+      // p = z + beta p - W nu, and the deferred x += alpha p_old of this iteration
+      if ((e = launch_prolong(A, P.nflags, D, W[c].nu, W[c].p, W[c].z, W[c].st, 1, s, P.xs[c])) != cudaSuccess)
+        return e;
+    }
+    return cudaSuccess;
   };
-  // TVB_SOLVE_PROFILE=1: run a few iterations eagerly with CUDA events around
-  // every stage and print the per-stage device time (tuning only).
-  if (getenv("TVB_SOLVE_PROFILE")) {
+  // TVB_SOLVE_PROFILE=1 (single RHS): run a few iterations eagerly with CUDA
+  // events around every stage and print the per-stage device time (tuning only).
+  if (getenv("TVB_SOLVE_PROFILE") && m == 1) {
     const char* names[6] = {"matvec_Ap+pq", "pcg_update", "matvec_Az", "restrict", "coarse_solve", "nu+prolong"};
     double acc[6] = {0, 0, 0, 0, 0, 0};
     cudaEvent_t ev[7];
     for (auto& e : ev) cudaEventCreate(&e);
+    const int* stop = &W[0].st->done;
     int nit = 0;
     for (; nit < 20; ++nit) {
       cudaEventRecord(ev[0], s);
-      matvec(W.p, W.q, true, stop);
+      matvec(0, W[0].p, W[0].q, true, stop);
       cudaEventRecord(ev[1], s);
-      launch_pcg_update(nd, defl ? nullptr : P.x, W.r, W.z, W.p, W.q, W.inv_d, W.st, W.partials,
-                        W.partials + 2 * kMaxReduceCtas, plan.nblocks(), s);
+      launch_pcg_update(nd, defl ? nullptr : P.xs[0], W[0].r, W[0].z, W[0].p, W[0].q, inv_d, W[0].st,
+                        W[0].partials, W[0].partials + 2 * kMaxReduceCtas, plan.nblocks(), s);
       cudaEventRecord(ev[2], s);
       if (defl) {
-        matvec(W.z, W.t, false, stop);
+        matvec(0, W[0].z, W[0].t, false, stop);
         cudaEventRecord(ev[3], s);
-        launch_restrict(A, P.nflags, D, W.t, W.yc, s, stop, W.q, W.st);
+        launch_restrict(A, P.nflags, D, W[0].t, W[0].yc, s, stop, W[0].q, W[0].st);
         cudaEventRecord(ev[4], s);
-        if (P.coarse_kind == 1) launch_coarse_nd(P.nd, W.yc, W.mu, stop, s);
-        else launch_dense_gemv(6 * A.nb, P.coarse, W.yc, W.mu, stop, s);
+        coarse_solve(0, 1, stop);
         cudaEventRecord(ev[5], s);
-        launch_block_nu(A, D, W.mu, W.nu, s, stop);
-        launch_prolong(A, P.nflags, D, W.nu, W.p, W.z, W.st, 1, s, P.x);
+        launch_block_nu(A, D, W[0].mu, W[0].nu, s, stop);
+        launch_prolong(A, P.nflags, D, W[0].nu, W[0].p, W[0].z, W[0].st, 1, s, P.xs[0]);
       } else {
-        launch_pcg_pupdate(nd, W.p, W.z, W.st, s);
+        launch_pcg_pupdate(nd, W[0].p, W[0].z, W[0].st, s);
         for (int k = 3; k < 6; ++k) cudaEventRecord(ev[k], s);
       }
       cudaEventRecord(ev[6], s);
@@ -333,31 +423,55 @@ int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
     }
   } gguard{graph, exec};
 
+  SolverState hst[kPcgMaxRhs];
   int iters_launched = 0;
   while (true) {
     TVB_CK(cudaGraphLaunch(exec, s));
     iters_launched += batch;
-    TVB_CK(cudaMemcpyAsync(&hst, W.st, sizeof(hst), cudaMemcpyDeviceToHost, s));
+    for (int c = c_lo; c < c_hi; ++c)
+      if (active[c]) TVB_CK(cudaMemcpyAsync(&hst[c], W[c].st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
     TVB_CK(cudaStreamSynchronize(s));
-    if (hst.done) break;
+    bool all_done = true;
+    for (int c = c_lo; c < c_hi; ++c) all_done = all_done && (!active[c] || hst[c].done);
+    if (all_done) break;
     if (iters_launched > P.max_iters + batch) {
       set_last_error("solver state did not terminate");
       return kStatusCuda;
     }
   }
-  // the stopping iteration's x += alpha p rode on its (skipped) prolongation
-  if (defl && hst.iter > 0) TVB_CK(launch_x_finish(nd, P.x, W.p, W.st, s));
-  R.iterations = hst.iter;
-  R.residual = hst.res;
-  if (hst.done == 2) {
-    char buf[160];
-    snprintf(buf, sizeof(buf), "CG did not reach %g in %d iterations (residual %.3e)", P.tol, P.max_iters, hst.res);
-    set_last_error(buf);
-    return kStatusNoConvergence;
+  int status = kStatusOk;
+  for (int c = 0; c < m; ++c) {
+    if (!active[c]) {
+      if (rstat[c] != kStatusOk && status == kStatusOk) status = rstat[c];
+      continue;
+    }
+    // the stopping iteration's x += alpha p rode on its (skipped) prolongation
+    if (defl && hst[c].iter > 0) TVB_CK(launch_x_finish(nd, P.xs[c], W[c].p, W[c].st, s));
+    R[c].iterations = hst[c].iter;
+    R[c].residual = hst[c].res;
+    if (hst[c].done == 2) {
+      char buf[160];
+      snprintf(buf, sizeof(buf), "CG did not reach %g in %d iterations (residual %.3e)", P.tol, P.max_iters,
+               hst[c].res);
+      set_last_error(buf);
+      rstat[c] = kStatusNoConvergence;
+      if (status == kStatusOk) status = kStatusNoConvergence;
+      continue;
+    }
+    TVB_CK(launch_zero_fixed(G.nn, P.xs[c], P.nflags, s));
   }
-  TVB_CK(launch_zero_fixed(G.nn, P.x, P.nflags, s));
   TVB_CK(cudaStreamSynchronize(s));
-  return kStatusOk;
+  return status;
+}
+
+int pcg_solve(const PcgProblem& P, PcgResult& R, cudaStream_t user_stream) {
+  PcgProblem Q = P;
+  Q.nrhs = 1;
+  Q.fs[0] = P.f;
+  Q.xs[0] = P.x;
+  int st1 = 0;
+  const int st = pcg_solve_multi(Q, &R, &st1, user_stream);
+  return st;
 }
 
 }  // namespace tvb

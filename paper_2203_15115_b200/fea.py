@@ -192,11 +192,11 @@ class StiffnessOperator:
             self._diag = self.diagonal_device().cpu().numpy()
         return self._diag
 
-    def pcg_workspace(self, block: int):
+    def pcg_workspace(self, block: int, nrhs: int = 1):
         torch = _torch()
-        key = int(block)
+        key = (int(block), int(nrhs))
         if key not in self._pcg_ws:
-            n = lib().tvb_pcg_ws_bytes(*self._dims(), key)
+            n = lib().tvb_pcg_batch_ws_bytes(*self._dims(), int(block), int(nrhs))
             self._pcg_ws[key] = torch.empty(n, dtype=torch.uint8, device="cuda")
         return self._pcg_ws[key]
 
@@ -411,15 +411,27 @@ def solve_static(op: StiffnessOperator, f, tol: float = 1.0e-8, max_iters: int |
     defl = deflation if (deflation is not None and deflation.n_vectors > 0) else None
     if defl is not None:
         defl.prepare(op)
-    d = op.domain
     x = torch.empty(op.n_dofs, dtype=torch.float64, device="cuda")
-    block = defl.block if defl is not None else 0
-    ws = op.pcg_workspace(block)
+    ws = op.pcg_workspace(defl.block if defl is not None else 0)
+    desc = _pcg_desc(op, defl, tol, max_iters, check_every, ws)
+    desc.d_f, desc.d_x = ptr(f_d), ptr(x)
+    st = lib().tvb_pcg_solve(ctypes.byref(desc), stream_ptr())
+    if st == STATUS_NO_CONVERGENCE:
+        raise NoConvergence(f"CG did not reach {tol:g} in {max_iters} iterations (residual {desc.residual:.3e})",
+                            residual=desc.residual, iterations=max_iters)
+    if st != 0:
+        raise_for_status(st, "solve_static", _lib.last_error())
+    return SolveResult(to_host_if(x, np_in), int(desc.iterations), float(desc.residual))
+
+
+def _pcg_desc(op: StiffnessOperator, defl, tol: float, max_iters: int, check_every: int, ws):
+    """tvb_pcg_desc of the operator / deflation space (RHS pointers unset)."""
+    d = op.domain
     desc = _lib.PcgDesc()
     desc.nx, desc.ny, desc.nz, desc.h = d.nx, d.ny, d.nz, d.h
     desc.h_mh45 = op.mh.ctypes.data
     desc.h_kdiag3 = op._kdiag.ctypes.data
-    desc.d_occ, desc.d_nflags, desc.d_f, desc.d_x = ptr(op.occ_d), ptr(op.nflags), ptr(f_d), ptr(x)
+    desc.d_occ, desc.d_nflags = ptr(op.occ_d), ptr(op.nflags)
     desc.d_ws, desc.ws_bytes = ptr(ws), ws.numel()
     desc.tol, desc.max_iters, desc.check_every = float(tol), int(max_iters), int(check_every)
     if defl is not None:
@@ -431,13 +443,71 @@ def solve_static(op: StiffnessOperator, f, tol: float = 1.0e-8, max_iters: int |
         else:
             desc.d_coarse = ptr(defl.coarse_inv)
             desc.coarse_kind = 0
-    st = lib().tvb_pcg_solve(ctypes.byref(desc), stream_ptr())
-    if st == STATUS_NO_CONVERGENCE:
-        raise NoConvergence(f"CG did not reach {tol:g} in {max_iters} iterations (residual {desc.residual:.3e})",
-                            residual=desc.residual, iterations=max_iters)
-    if st != 0:
-        raise_for_status(st, "solve_static", _lib.last_error())
-    return SolveResult(to_host_if(x, np_in), int(desc.iterations), float(desc.residual))
+    return desc
+
+
+#: right-hand sides per batched device solve (solver.cuh kPcgMaxRhs)
+MAX_BATCH_RHS = 8
+
+
+def solve_static_batch(op: StiffnessOperator, forces, tol: float = 1.0e-8, max_iters: int | None = None,
+                       deflation: DeflationSpace | None = None, check_every: int = 8) -> list:
+    """Multi-RHS batching: solve K u_c = f_c for several load
+    vectors against ONE operator and deflation space -- every load case and
+    adjoint of a topology. Each RHS follows ``solve_static`` exactly (own
+    stopping test, iteration count and errors; its result is bitwise the one
+    ``solve_static`` returns for it alone); per iteration the coarse solve
+    reads the factor once for all RHS and one CUDA graph launch / host check
+    serves them all.
+
+    ``forces``: a sequence of vectors or an (m, n_dofs) array / tensor.
+    Returns a list of ``SolveResult``. Raises like ``solve_static`` for the
+    first failing RHS (``NoConvergence`` carries that RHS's residual)."""
+    torch = _torch()
+    if not 0.0 < tol <= 1.0e-2:
+        raise ValueError(f"tolerance must lie in (0, 1e-2], got {tol}")
+    if isinstance(forces, torch.Tensor) or isinstance(forces, np.ndarray):
+        if forces.ndim != 2:
+            raise DimensionMismatch(f"force batch must be 2-D (m, n_dofs), got shape {tuple(forces.shape)}")
+        forces = [forces[i] for i in range(forces.shape[0])]
+    forces = list(forces)
+    if not forces:
+        return []
+    if max_iters is None:
+        max_iters = default_max_iters(op.n_dofs)
+    fds, np_flags = [], []
+    for i, f in enumerate(forces):
+        f_d, np_in = to_device(f, op.n_dofs, f"force vector {i}")
+        if not bool(torch.isfinite(f_d).all()):
+            raise ValueError(f"force vector {i} is not finite")
+        fds.append(f_d.contiguous())
+        np_flags.append(np_in)
+    defl = deflation if (deflation is not None and deflation.n_vectors > 0) else None
+    if defl is not None:
+        defl.prepare(op)
+    out = []
+    for g0 in range(0, len(fds), MAX_BATCH_RHS):
+        grp = fds[g0:g0 + MAX_BATCH_RHS]
+        m = len(grp)
+        xs = [torch.empty(op.n_dofs, dtype=torch.float64, device="cuda") for _ in range(m)]
+        ws = op.pcg_workspace(defl.block if defl is not None else 0, m)
+        desc = _pcg_desc(op, defl, tol, max_iters, check_every, ws)
+        fptr = (ctypes.c_void_p * m)(*[ptr(t) for t in grp])
+        xptr = (ctypes.c_void_p * m)(*[ptr(t) for t in xs])
+        its = (ctypes.c_int * m)()
+        res = (ctypes.c_double * m)()
+        sts = (ctypes.c_int * m)()
+        lib().tvb_pcg_solve_batch(ctypes.byref(desc), m, ctypes.cast(fptr, ctypes.c_void_p),
+                                  ctypes.cast(xptr, ctypes.c_void_p), ctypes.cast(its, ctypes.c_void_p),
+                                  ctypes.cast(res, ctypes.c_void_p), ctypes.cast(sts, ctypes.c_void_p), stream_ptr())
+        for c in range(m):
+            if sts[c] == STATUS_NO_CONVERGENCE:
+                raise NoConvergence(f"CG did not reach {tol:g} in {max_iters} iterations for right-hand side "
+                                    f"{g0 + c} (residual {res[c]:.3e})", residual=res[c], iterations=max_iters)
+            if sts[c] != 0:
+                raise_for_status(sts[c], f"solve_static_batch (right-hand side {g0 + c})", _lib.last_error())
+        out.extend(SolveResult(to_host_if(xs[c], np_flags[g0 + c]), int(its[c]), float(res[c])) for c in range(m))
+    return out
 
 
 def _solve_generic(op, f_d, tol, max_iters, apply_op, diag):
