@@ -331,33 +331,102 @@ int pcg_solve_multi(const PcgProblem& P, PcgResult* R, int* rstat, cudaStream_t 
   // 8 restriction, 16 coarse solve, 32 nu + prolongation; the in-graph cost of
   // a stage is the per-iteration time difference.
   const int skip = getenv("TVB_SOLVE_SKIP") ? atoi(getenv("TVB_SOLVE_SKIP")) : 0;
+  // Several RHS: each RHS's chain runs on its own capture stream (graph
+  // branch), so one RHS's small kernels overlap another's; the branches meet
+  // only at the shared coarse solve. TVB_BATCH_FORK=0 serialises them.
+  const bool fork = (c_hi - c_lo) > 1 && !(getenv("TVB_BATCH_FORK") && atoi(getenv("TVB_BATCH_FORK")) == 0);
+  cudaStream_t bs[kPcgMaxRhs];
+  cudaEvent_t ev_fork = nullptr, ev_branch[kPcgMaxRhs] = {};
+  int n_streams = 0;
+  struct ForkGuard {
+    cudaStream_t* s;
+    int* n;
+    cudaEvent_t* ev0;
+    cudaEvent_t* ev;
+    ~ForkGuard() {
+      for (int i = 0; i < *n; ++i) {
+        cudaStreamDestroy(s[i]);
+        if (ev[i]) cudaEventDestroy(ev[i]);
+      }
+      if (*ev0) cudaEventDestroy(*ev0);
+    }
+  } fguard{bs, &n_streams, &ev_fork, ev_branch};
+  if (fork) {
+    TVB_CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    for (int c = c_lo; c < c_hi; ++c) {
+      TVB_CK(cudaStreamCreateWithFlags(&bs[n_streams], cudaStreamNonBlocking));
+      TVB_CK(cudaEventCreateWithFlags(&ev_branch[n_streams], cudaEventDisableTiming));
+      ++n_streams;
+    }
+  }
+  auto sc = [&](int c) { return fork ? bs[c - c_lo] : s; };
+  // s -> every branch (fork) / every branch -> s (join)
+  auto fork_from_s = [&]() -> cudaError_t {
+    if (!fork) return cudaSuccess;
+    cudaError_t e = cudaEventRecord(ev_fork, s);
+    for (int c = c_lo; c < c_hi && e == cudaSuccess; ++c) e = cudaStreamWaitEvent(sc(c), ev_fork, 0);
+    return e;
+  };
+  auto join_to_s = [&]() -> cudaError_t {
+    if (!fork) return cudaSuccess;
+    cudaError_t e = cudaSuccess;
+    for (int c = c_lo; c < c_hi && e == cudaSuccess; ++c) {
+      e = cudaEventRecord(ev_branch[c - c_lo], sc(c));
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_branch[c - c_lo], 0);
+    }
+    return e;
+  };
   auto one_iteration = [&]() -> cudaError_t {
     cudaError_t e = cudaSuccess;
     for (int c = c_lo; c < c_hi; ++c) {
       const int* stop = &W[c].st->done;
-      if (!(skip & 1) && (e = matvec(c, W[c].p, W[c].q, true, stop)) != cudaSuccess) return e;
+      cudaStream_t cs = sc(c);
+      MatvecParams mp{};
+      if (!(skip & 1)) {
+        mp.g = G;
+        mp.u = W[c].p;
+        mp.y = W[c].q;
+        mp.occ = P.occ;
+        mp.fixed = P.nflags;
+        mp.mask_out = 1;
+        mp.dot_partial = W[c].partials + 2 * kMaxReduceCtas;
+        mp.stop = stop;
+        if ((e = launch_matvec(plan, mp, P.modal, cs)) != cudaSuccess) return e;
+      }
       if (!(skip & 2) &&
           (e = launch_pcg_update(nd, defl ? nullptr : P.xs[c], W[c].r, W[c].z, W[c].p, W[c].q, inv_d, W[c].st,
-                                 W[c].partials, W[c].partials + 2 * kMaxReduceCtas, plan.nblocks(), s)) !=
+                                 W[c].partials, W[c].partials + 2 * kMaxReduceCtas, plan.nblocks(), cs)) !=
               cudaSuccess)
         return e;
       if (!defl) {
-        if ((e = launch_pcg_pupdate(nd, W[c].p, W[c].z, W[c].st, s)) != cudaSuccess) return e;
+        if ((e = launch_pcg_pupdate(nd, W[c].p, W[c].z, W[c].st, cs)) != cudaSuccess) return e;
         continue;
       }
-      if (!(skip & 4) && (e = matvec(c, W[c].z, W[c].t, false, stop)) != cudaSuccess) return e;
+      if (!(skip & 4)) {
+        mp = MatvecParams{};
+        mp.g = G;
+        mp.u = W[c].z;
+        mp.y = W[c].t;
+        mp.occ = P.occ;
+        mp.fixed = P.nflags;
+        mp.mask_out = 1;
+        mp.stop = stop;
+        if ((e = launch_matvec(plan, mp, P.modal, cs)) != cudaSuccess) return e;
+      }
       if (!(skip & 8) &&
-          (e = launch_restrict(A, P.nflags, D, W[c].t, W[c].yc, s, stop, W[c].q, W[c].st)) != cudaSuccess)
+          (e = launch_restrict(A, P.nflags, D, W[c].t, W[c].yc, cs, stop, W[c].q, W[c].st)) != cudaSuccess)
         return e;
     }
     if (!defl) return cudaSuccess;
+    if ((e = join_to_s()) != cudaSuccess) return e;
     if (!(skip & 16) && (e = coarse_solve(c_lo, c_hi - c_lo, &W[c_lo].st->done)) != cudaSuccess) return e;
+    if ((e = fork_from_s()) != cudaSuccess) return e;
     if (skip & 32) return cudaSuccess;
     for (int c = c_lo; c < c_hi; ++c) {
       const int* stop = &W[c].st->done;
-      if ((e = launch_block_nu(A, D, W[c].mu, W[c].nu, s, stop)) != cudaSuccess) return e;
+      if ((e = launch_block_nu(A, D, W[c].mu, W[c].nu, sc(c), stop)) != cudaSuccess) return e;
       // p = z + beta p - W nu, and the deferred x += alpha p_old of this iteration
-      if ((e = launch_prolong(A, P.nflags, D, W[c].nu, W[c].p, W[c].z, W[c].st, 1, s, P.xs[c])) != cudaSuccess)
+      if ((e = launch_prolong(A, P.nflags, D, W[c].nu, W[c].p, W[c].z, W[c].st, 1, sc(c), P.xs[c])) != cudaSuccess)
         return e;
     }
     return cudaSuccess;
@@ -408,8 +477,9 @@ int pcg_solve_multi(const PcgProblem& P, PcgResult* R, int* rstat, cudaStream_t 
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   TVB_CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  cudaError_t cap = cudaSuccess;
+  cudaError_t cap = fork_from_s();
   for (int i = 0; i < batch && cap == cudaSuccess; ++i) cap = one_iteration();
+  if (cap == cudaSuccess) cap = join_to_s();
   cudaError_t endcap = cudaStreamEndCapture(s, &graph);
   TVB_CK(cap);
   TVB_CK(endcap);

@@ -180,48 +180,56 @@ class Analyses:
         self.fields = {}
         self.J = {}
         self.solves = 0
-        ops = {}
         cases = {c.id: c for c in problem.load_cases}
+        for name, spec in specs.items():
+            if spec.load_case not in ("", *cases):
+                raise MissingAnalysis(f"constraint {name!r} refers to unknown load case {spec.load_case!r}")
+            if spec.kind == "displacement" and spec.dof is None:
+                raise SemanticError(f"displacement constraint {name!r} needs a dof")
+        # load cases sharing a Dirichlet set share one operator / deflation
+        # space and are solved together (multi-RHS batch, fea.solve_static_batch);
+        # so are their adjoint right-hand sides
+        groups = {}
         for case in problem.load_cases:
             fixed, f = _case_data(problem, case)
             key = fixed.tobytes()
-            if key not in ops:
+            if key not in groups:
                 op = fea.StiffnessOperator(d, topology, problem.material, fixed)
                 defl = fea.build_deflation(d, topology, fixed, cfg.block) if cfg.block else None
-                ops[key] = (op, defl)
-            op, defl = ops[key]
-            u = fea.solve_static(op, f, tol=cfg.tol, deflation=defl).u
-            self.solves += 1
-            self.J[case.id] = float(f @ u)
-            vm, tj, _ = sensitivity.element_fields_device(op, u, 2)
-            for name, spec in specs.items():
-                if spec.load_case not in ("", case.id) and spec.load_case not in cases:
-                    raise MissingAnalysis(f"constraint {name!r} refers to unknown load case {spec.load_case!r}")
-                if (spec.load_case or problem.load_cases[0].id) != case.id:
-                    continue
-                if spec.kind == "compliance":
-                    self.q[name] = self.J[case.id]
-                    if need_fields:
-                        self.fields[name] = tj
-                elif spec.kind == "pnorm_stress":
-                    _, _, sums = sensitivity.element_fields_device(op, u, spec.p)
-                    s = sums.cpu().numpy()
-                    self.q[name] = float((s[0] / s[1]) ** (1.0 / spec.p))
-                    if need_fields:
-                        rhs = sensitivity.adjoint_rhs_device(op, u, spec.p, sums)
-                        lam = fea.solve_static(op, rhs, tol=cfg.tol, deflation=defl).u
-                        self.solves += 1
-                        self.fields[name] = sensitivity.stress_sensitivity(op, u, lam)
-                elif spec.kind == "displacement":
-                    if spec.dof is None:
-                        raise SemanticError(f"displacement constraint {name!r} needs a dof")
-                    self.q[name] = abs(float(u[spec.dof]))
-                    if need_fields:
-                        e = torch.zeros_like(u)
-                        e[spec.dof] = math.copysign(1.0, float(u[spec.dof]))
-                        lam = fea.solve_static(op, e, tol=cfg.tol, deflation=defl).u
-                        self.solves += 1
-                        self.fields[name] = sensitivity.stress_sensitivity(op, u, lam)
+                groups[key] = (op, defl, [])
+            groups[key][2].append((case, f))
+        for op, defl, members in groups.values():
+            sols = fea.solve_static_batch(op, [f for _, f in members], tol=cfg.tol, deflation=defl)
+            self.solves += len(members)
+            adjoints = []  # (constraint name, u, adjoint rhs)
+            for (case, f), sol in zip(members, sols):
+                u = sol.u
+                self.J[case.id] = float(f @ u)
+                vm, tj, _ = sensitivity.element_fields_device(op, u, 2)
+                for name, spec in specs.items():
+                    if (spec.load_case or problem.load_cases[0].id) != case.id:
+                        continue
+                    if spec.kind == "compliance":
+                        self.q[name] = self.J[case.id]
+                        if need_fields:
+                            self.fields[name] = tj
+                    elif spec.kind == "pnorm_stress":
+                        _, _, sums = sensitivity.element_fields_device(op, u, spec.p)
+                        s = sums.cpu().numpy()
+                        self.q[name] = float((s[0] / s[1]) ** (1.0 / spec.p))
+                        if need_fields:
+                            adjoints.append((name, u, sensitivity.adjoint_rhs_device(op, u, spec.p, sums)))
+                    elif spec.kind == "displacement":
+                        self.q[name] = abs(float(u[spec.dof]))
+                        if need_fields:
+                            e = torch.zeros_like(u)
+                            e[spec.dof] = math.copysign(1.0, float(u[spec.dof]))
+                            adjoints.append((name, u, e))
+            if adjoints:
+                lams = fea.solve_static_batch(op, [rhs for _, _, rhs in adjoints], tol=cfg.tol, deflation=defl)
+                self.solves += len(adjoints)
+                for (name, u, _), lam in zip(adjoints, lams):
+                    self.fields[name] = sensitivity.stress_sensitivity(op, u, lam.u)
         self.J_total = float(sum(self.J.values()))
 
 
