@@ -278,6 +278,7 @@ def main():
     }
     if rank == 0 and not args.no_secondary:
         line["secondary"] = secondary_solves(tv, fea, torch, p64, hbm)
+        line["secondary"]["C4_two_load_cases_batched"] = secondary_batch(tv, fea, torch)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_matvec(occ, u)
@@ -370,6 +371,45 @@ def secondary_solves(tv, fea, torch, p64, hbm):
         except Exception as exc:
             out[name] = {"error": repr(exc)[:300]}
     return out
+
+
+def secondary_batch(tv, fea, torch):
+    """Multi-RHS batching: the two load cases of BASELINE
+    configs[3] ((0,0,-1) and (0,-1,0) over the 3x3 patch of the x=160 face) on
+    the full-solid C4 geometry, solved one after the other (solve_static) and
+    as one batch (solve_static_batch); device-timed, tol 1e-8."""
+    try:
+        d = tv.Domain(160, 80, 80, 1.0)
+        fs = []
+        for fv in ((0, 0, -1), (0, -1, 0)):
+            case = tv.LoadCase("c", dirichlet=((tv.RegionSelector("box", min=(0, 0, 0), max=(0, 80, 80)), (1, 1, 1)),),
+                               loads=((tv.RegionSelector("box", min=(160, 39, 39), max=(160, 41, 41)), fv, "total"),))
+            fs.append(torch.from_numpy(tv.assemble_force(d, case)).cuda())
+        fixed = tv.dirichlet_dofs(d, case)
+        op = fea.StiffnessOperator(d, tv.Topology(d, np.ones(d.n_elems)), tv.Material(E=1.0, nu=0.3), fixed)
+        defl = fea.build_deflation(d, op.topology, fixed, 8)
+        defl.prepare(op)
+        fea.solve_static_batch(op, fs, tol=1e-8, deflation=defl)  # warm
+        for f in fs:
+            fea.solve_static(op, f, tol=1e-8, deflation=defl)
+
+        def timed(fn):
+            a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record()
+            out = fn()
+            e.record()
+            torch.cuda.synchronize()
+            return a.elapsed_time(e), out
+
+        t_seq, rs = timed(lambda: [fea.solve_static(op, f, tol=1e-8, deflation=defl) for f in fs])
+        t_bat, rb = timed(lambda: fea.solve_static_batch(op, fs, tol=1e-8, deflation=defl))
+        its = [r.iterations for r in rb]
+        return {"iterations": its, "sequential_ms": t_seq, "batch_ms": t_bat, "speedup": t_seq / t_bat,
+                "us_per_rhs_iter": 1e3 * t_bat / sum(its),
+                "bitwise_equal_to_single": all(torch.equal(x.u, y.u) for x, y in zip(rs, rb))}
+    except Exception as exc:
+        return {"error": repr(exc)[:300]}
 
 
 if __name__ == "__main__":
