@@ -254,6 +254,21 @@ size_t tvb_select_ws_bytes(long long n);
 int tvb_threshold_select(const double* d_ls, const uint8_t* d_design, long long n, long long k, double ersatz,
                          double nondesign, double* d_occ, void* d_ws, size_t ws_bytes,
                          unsigned long long* h_state4, void* stream);
+/* extract with casting: flags bit 0 = retain EVERY design
+ * element whose value equals the threshold (the superlevel set {v >= tau} of a
+ * casting-projected field is undercut-free; the fraction may exceed the
+ * target). flags = 0 is tvb_threshold_select. */
+int tvb_threshold_select_ex(const double* d_ls, const uint8_t* d_design, long long n, long long k, double ersatz,
+                            double nondesign, int flags, double* d_occ, void* d_ws, size_t ws_bytes,
+                            unsigned long long* h_state4, void* stream);
+/* casting_project (PAPER §3.7): along each element column
+ * parallel to axis (0 = x, 1 = y, 2 = z), running minimum moving away from the
+ * parting plane. Element layers i >= parting form the +axis mold half, i <
+ * parting the -axis half; parting in [0, n_axis] (0 = one +axis half, n_axis =
+ * one -axis half). d_in == d_out allowed. Replaces no reference code (the
+ * reference ships none); oracle/topovox_oracle.py:casting_project. */
+int tvb_casting_project(int nx, int ny, int nz, int axis, int parting, const double* d_in, double* d_out,
+                        void* stream);
 
 #ifdef __cplusplus
 }

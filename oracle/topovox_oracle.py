@@ -444,9 +444,10 @@ def extract_count(target_vf, n_design):
     return int(min(max(np.floor(target_vf * n_design + 0.5), 0), n_design))
 
 
-def extract(levelset, design_mask, target_vf, ersatz):
+def extract(levelset, design_mask, target_vf, ersatz, all_ties=False):
     """SPEC.md:396 order-statistic threshold over design elements; equal
-    values are taken in ascending element index. Returns (occ, tau, k)."""
+    values are taken in ascending element index (all_ties: every design
+    element equal to the threshold, the casting mode). Returns (occ, tau, k)."""
     ls = np.asarray(levelset, dtype=float)
     idx = np.flatnonzero(design_mask)
     k = extract_count(target_vf, idx.size)
@@ -455,7 +456,40 @@ def extract(levelset, design_mask, target_vf, ersatz):
     chosen = idx[order[:k]]
     occ[chosen] = 1.0
     tau = ls[idx[order[k - 1]]] if k > 0 else np.inf
+    if all_ties and k > 0:
+        occ[idx[ls[idx] == tau]] = 1.0
     return occ, tau, k
+
+
+def casting_project(field, dims, axis, parting):
+    """SPEC.md:402-410 (PAPER §3.7): along every element column parallel to
+    `axis` (0/1/2), the running minimum moving away from the parting plane;
+    element layers >= parting are the +axis mold half, < parting the -axis
+    half. Field in element order e = x + nx (y + ny z)."""
+    nx, ny, nz = dims
+    f = np.asarray(field, dtype=float).reshape(nz, ny, nx)  # [z, y, x]
+    ax = 2 - axis
+    f = np.moveaxis(f, ax, 0).copy()  # [axis, ...]
+    if parting < f.shape[0]:
+        f[parting:] = np.minimum.accumulate(f[parting:], axis=0)
+    if parting > 0:
+        f[:parting] = np.minimum.accumulate(f[:parting][::-1], axis=0)[::-1]
+    return np.moveaxis(f, 0, ax).reshape(-1)
+
+
+def undercut_violations(occ, dims, axis, parting):
+    """Exhaustive column audit: per column and mold half,
+    the occupied cells (occ == 1) must form one run starting at the parting
+    plane. Returns the number of violating (column, half) pairs."""
+    nx, ny, nz = dims
+    o = np.moveaxis((np.asarray(occ) == 1.0).reshape(nz, ny, nx), 2 - axis, 0)
+    bad = 0
+    for half in (o[parting:], o[:parting][::-1]):
+        if half.shape[0] == 0:
+            continue
+        run = np.logical_and.accumulate(half, axis=0)  # contiguous from the plane
+        bad += int(np.any(half != run, axis=0).sum())
+    return bad
 
 
 # --- augmented Lagrangian scalars (SPEC.md:466-501) --------------------------
@@ -509,8 +543,9 @@ def _analyses(nx, ny, nz, occ, cases, specs, E, nu, tol, block, need_fields=True
 
 def run_optimizer(nx, ny, nz, cases, specs, E=1.0, nu=0.3, tol=1e-8, block=4, ersatz=1e-6, mu0=100.0, gamma0=10.0,
                   varsigma=0.25, eta=10.0, dv0=0.025, dv_min=0.005, growth=1.1, growth_after=3, inner_cap=10,
-                  ctol=0.01, ttol=0.001, feas=1e-6, max_outer=400):
-    """Returns (occ, history list of dicts, reason)."""
+                  ctol=0.01, ttol=0.001, feas=1e-6, max_outer=400, casting=None):
+    """Returns (occ, history list of dicts, reason). casting: (axis, parting
+    element layer) -> casting-projected extraction with all ties retained."""
     ne = nx * ny * nz
     design = np.ones(ne, dtype=bool)
     occ = np.ones(ne)
@@ -536,7 +571,9 @@ def run_optimizer(nx, ny, nz, cases, specs, E=1.0, nu=0.3, tol=1e-8, block=4, er
             inner = it
             ls, _ = combine([cur["fields"][i] for i in range(len(specs))], [w[i] for i in range(len(specs))],
                             fallback=fb)
-            new_occ, _, _ = extract(ls, design, target, ersatz)
+            if casting is not None:
+                ls = casting_project(ls, (nx, ny, nz), *casting)
+            new_occ, _, _ = extract(ls, design, target, ersatz, all_ties=casting is not None)
             if it > 1 and np.count_nonzero((new_occ == 1.0) != (cur_occ == 1.0)) < ttol * ne:
                 conv = True
                 break

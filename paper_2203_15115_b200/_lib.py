@@ -90,6 +90,8 @@ _SIGS = {
     "tvb_combine": (c_int, [c_int, P, P, P, c_ll, P, P]),
     "tvb_select_ws_bytes": (c_size_t, [c_ll]),
     "tvb_threshold_select": (c_int, [P, P, c_ll, c_ll, c_double, c_double, P, P, c_size_t, P, P]),
+    "tvb_threshold_select_ex": (c_int, [P, P, c_ll, c_ll, c_double, c_double, c_int, P, P, c_size_t, P, P]),
+    "tvb_casting_project": (c_int, [c_int, c_int, c_int, c_int, c_int, P, P, P]),
 }
 
 MASK_IN, MASK_OUT, ACCUMULATE = 1, 2, 4

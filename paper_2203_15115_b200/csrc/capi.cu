@@ -678,15 +678,32 @@ int tvb_combine(int k, const double* const* h_fields, const double* h_w, const d
 
 size_t tvb_select_ws_bytes(long long n) { return select_ws_bytes(n); }
 
+int tvb_threshold_select_ex(const double* d_ls, const uint8_t* d_design, long long n, long long k, double ersatz,
+                            double nondesign, int flags, double* d_occ, void* d_ws, size_t ws_bytes,
+                            unsigned long long* h_state4, void* stream) {
+  if (!d_ls || !d_occ || n < 1 || k < 0 || k > n || (flags & ~1)) return kStatusBadArg;
+  if (!d_ws || ws_bytes < select_ws_bytes(n)) return kStatusWorkspace;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int st = check(launch_select(d_ls, d_design, n, k, ersatz, nondesign, d_occ, d_ws, h_state4, s, flags & 1)))
+    return st;
+  if (h_state4) return check(cudaStreamSynchronize(s));
+  return kStatusOk;
+}
+
 int tvb_threshold_select(const double* d_ls, const uint8_t* d_design, long long n, long long k, double ersatz,
                          double nondesign, double* d_occ, void* d_ws, size_t ws_bytes, unsigned long long* h_state4,
                          void* stream) {
-  if (!d_ls || !d_occ || n < 1 || k < 0 || k > n) return kStatusBadArg;
-  if (!d_ws || ws_bytes < select_ws_bytes(n)) return kStatusWorkspace;
-  cudaStream_t s = (cudaStream_t)stream;
-  if (int st = check(launch_select(d_ls, d_design, n, k, ersatz, nondesign, d_occ, d_ws, h_state4, s))) return st;
-  if (h_state4) return check(cudaStreamSynchronize(s));
-  return kStatusOk;
+  return tvb_threshold_select_ex(d_ls, d_design, n, k, ersatz, nondesign, 0, d_occ, d_ws, ws_bytes, h_state4,
+                                 stream);
+}
+
+int tvb_casting_project(int nx, int ny, int nz, int axis, int parting, const double* d_in, double* d_out,
+                        void* stream) {
+  if (bad_dims(nx, ny, nz) || axis < 0 || axis > 2 || !d_in || !d_out) return kStatusBadArg;
+  const Grid G = make_grid(nx, ny, nz);
+  const int na = axis == 0 ? nx : axis == 1 ? ny : nz;
+  if (parting < 0 || parting > na) return kStatusBadArg;
+  return check(launch_casting_project(G, axis, parting, d_in, d_out, (cudaStream_t)stream));
 }
 
 }  // extern "C"

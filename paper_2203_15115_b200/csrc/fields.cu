@@ -302,9 +302,10 @@ __global__ void k_scan_counts(unsigned int* bcount, int nb) {
 }
 
 // occ = 1 for key > tau, or key == tau among the first (k - #greater) by index
+// (all_ties: every key == tau -- casting extraction, "best-feasible")
 __global__ void k_apply_threshold(const double* ls, const uint8_t* design, long long n,
                                   const unsigned long long* state, const unsigned int* boff, double ersatz,
-                                  double nondesign, double* occ) {
+                                  double nondesign, double* occ, int all_ties) {
   __shared__ unsigned int flags[1024];
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const bool in = i < n;
@@ -325,12 +326,61 @@ __global__ void k_apply_threshold(const double* ls, const uint8_t* design, long 
   const unsigned long long rank = boff[blockIdx.x] + flags[threadIdx.x] - (eq ? 1u : 0u);
   double v;
   if (!des) v = nondesign;
-  else if (k > tau || (eq && rank < need)) v = 1.0;
+  else if (k > tau || (eq && (all_ties || rank < need))) v = 1.0;
   else v = ersatz;
   occ[i] = v;
 }
 
 // ---------------------------------------------------------------------------
+// casting projection (§3.7): along every element column
+// parallel to `axis`, replace values by the running minimum moving away from
+// the parting plane -- element layers i >= P form the +axis mold half (walked
+// upwards), i < P the -axis half (walked downwards). One thread per column;
+// consecutive threads take consecutive columns of the fastest non-axis
+// dimension, so for axis y / z every step is a coalesced row. In place is
+// allowed (each value is read before its own thread writes it).
+// ---------------------------------------------------------------------------
+__global__ void k_casting_project(Grid G, int axis, int P, const double* in, double* out) {
+  const long long ncol = axis == 0 ? (long long)G.ny * G.nz : axis == 1 ? (long long)G.nx * G.nz
+                                                                       : (long long)G.nx * G.ny;
+  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (c >= ncol) return;
+  long long base, stride;
+  int na;
+  if (axis == 0) {
+    base = c * G.nx;  // (y, z) -> row start
+    stride = 1;
+    na = G.nx;
+  } else if (axis == 1) {
+    const long long x = c % G.nx, z = c / G.nx;
+    base = x + (long long)G.nx * G.ny * z;
+    stride = G.nx;
+    na = G.ny;
+  } else {
+    base = c;  // (x, y)
+    stride = (long long)G.nx * G.ny;
+    na = G.nz;
+  }
+  double m = 0.0;
+  for (int i = P; i < na; ++i) {  // +axis half
+    const double v = in[base + stride * i];
+    m = (i == P || v < m) ? v : m;
+    out[base + stride * i] = m;
+  }
+  for (int i = P - 1; i >= 0; --i) {  // -axis half
+    const double v = in[base + stride * i];
+    m = (i == P - 1 || v < m) ? v : m;
+    out[base + stride * i] = m;
+  }
+}
+
+cudaError_t launch_casting_project(const Grid& G, int axis, int P, const double* in, double* out, cudaStream_t s) {
+  const long long ncol = axis == 0 ? (long long)G.ny * G.nz : axis == 1 ? (long long)G.nx * G.nz
+                                                                       : (long long)G.nx * G.ny;
+  k_casting_project<<<(unsigned)((ncol + 127) / 128), 128, 0, s>>>(G, axis, P, in, out);
+  return cudaGetLastError();
+}
+
 int elem_grid(long long n) { return (int)((n + 255) / 256); }
 
 cudaError_t launch_element_state(const ElemArgs& A, cudaStream_t s) {
@@ -390,7 +440,8 @@ size_t select_ws_bytes(long long n) {
 }
 
 cudaError_t launch_select(const double* ls, const uint8_t* design, long long n, long long k, double ersatz,
-                          double nondesign, double* occ, void* ws, unsigned long long* state_out, cudaStream_t s) {
+                          double nondesign, double* occ, void* ws, unsigned long long* state_out, cudaStream_t s,
+                          int all_ties) {
   unsigned long long* state = (unsigned long long*)ws;
   unsigned int* hist = (unsigned int*)((char*)ws + 64);
   unsigned int* bcount = hist + 256;
@@ -415,7 +466,8 @@ cudaError_t launch_select(const double* ls, const uint8_t* design, long long n, 
   }
   k_eq_count<<<nb, 1024, 0, s>>>(ls, design, n, state, bcount);
   k_scan_counts<<<1, 1024, 0, s>>>(bcount, nb);
-  k_apply_threshold<<<nb, 1024, 0, s>>>(ls, design, n, state, bcount, ersatz, nondesign, occ);
+  k_apply_threshold<<<nb, 1024, 0, s>>>(ls, design, n, state, bcount, ersatz, nondesign, occ,
+                                        k > 0 ? all_ties : 0);
   if (state_out) {
     e = cudaMemcpyAsync(state_out, state, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return e;

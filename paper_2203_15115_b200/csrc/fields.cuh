@@ -43,6 +43,9 @@ cudaError_t launch_maxabs(const double* t, long long n, double* partials, double
 cudaError_t launch_combine(const CombineArgs& C, long long n, double* out, cudaStream_t s);
 size_t select_ws_bytes(long long n);
 cudaError_t launch_select(const double* ls, const uint8_t* design, long long n, long long k, double ersatz,
-                          double nondesign, double* occ, void* ws, unsigned long long* state_out, cudaStream_t s);
+                          double nondesign, double* occ, void* ws, unsigned long long* state_out, cudaStream_t s,
+                          int all_ties = 0);
+// casting projection along axis (0/1/2); element layers >= P form the +axis half
+cudaError_t launch_casting_project(const Grid& G, int axis, int P, const double* in, double* out, cudaStream_t s);
 
 }  // namespace tvb

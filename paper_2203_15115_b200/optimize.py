@@ -96,6 +96,7 @@ class Problem:
     material: Material
     load_cases: list
     constraints: list
+    casting: object = None  # levelset.CastingSpec (PAPER §3.7) or None
 
 
 @dataclass
@@ -260,7 +261,7 @@ def fixed_point(problem: Problem, specs: dict, start: Analyses, target_vf: float
         else:
             keep = [(cur.fields[n], x) for n, x in zip(names, w) if x != 0.0]
             ls = combine_device([k for k, _ in keep], [x for _, x in keep])
-        occ_d, _, _ = extract_device(problem.domain, ls, target_vf, cfg.ersatz, design)
+        occ_d, _, _ = extract_device(problem.domain, ls, target_vf, cfg.ersatz, design, casting=problem.casting)
         occ = occ_d.cpu().numpy()
         changed = int(np.count_nonzero((occ == 1.0) != (prev_occ == 1.0)))
         if it > 1 and changed < cfg.topology_tol * problem.domain.n_elems:

@@ -118,3 +118,33 @@ def test_adjoint_rhs_finite_difference(oracle):
         e[i] = h
         fd = (spn(u + e) - spn(u - e)) / (2 * h)
         assert abs(fd - g[i]) <= 1e-4 * np.abs(g).max()
+
+
+def test_spec_casting_kats(oracle):
+    """SPEC.md:402-410 casting_project examples + invariants (idempotence,
+    undercut audit after extraction at 20 random thresholds)."""
+    # column (plane -> outward) [0.5, 0.2, 0.7] -> [0.5, 0.2, 0.2], along each axis
+    for axis, dims in ((0, (3, 1, 1)), (1, (1, 3, 1)), (2, (1, 1, 3))):
+        out = oracle.casting_project([0.5, 0.2, 0.7], dims, axis, 0)
+        assert np.array_equal(out, [0.5, 0.2, 0.2])
+        # the -axis half walks downwards from the plane
+        out = oracle.casting_project([0.7, 0.2, 0.5], dims, axis, 3)
+        assert np.array_equal(out, [0.2, 0.2, 0.5])
+    # two halves, plane at layer 2: [.3 .9 | .8 .1 .4] -> [.3 .9 | .8 .1 .1]
+    out = oracle.casting_project([0.3, 0.9, 0.8, 0.1, 0.4], (5, 1, 1), 0, 2)
+    assert np.array_equal(out, [0.3, 0.9, 0.8, 0.1, 0.1])
+    rng = np.random.default_rng(0)
+    dims = (7, 5, 6)
+    f = rng.standard_normal(7 * 5 * 6)
+    for axis in range(3):
+        for parting in (0, 2, dims[axis]):
+            p1 = oracle.casting_project(f, dims, axis, parting)
+            assert np.array_equal(oracle.casting_project(p1, dims, axis, parting), p1)  # idempotent
+            assert np.all(p1 <= f)
+            design = np.ones(f.size, dtype=bool)
+            for vf in rng.random(20):
+                occ, _, _ = oracle.extract(p1, design, max(vf, 0.02), 1e-3, all_ties=True)
+                assert oracle.undercut_violations(occ, dims, axis, parting) == 0
+    # monotone columns are unchanged
+    mono = np.repeat(np.arange(6, 0, -1, dtype=float), 35).reshape(6, 5, 7).reshape(-1)
+    assert np.array_equal(oracle.casting_project(mono, dims, 2, 0), mono)
