@@ -270,6 +270,30 @@ int tvb_threshold_select_ex(const double* d_ls, const uint8_t* d_design, long lo
 int tvb_casting_project(int nx, int ny, int nz, int axis, int parting, const double* d_in, double* d_out,
                         void* stream);
 
+/* ---- eigen / buckling ---------- */
+/* apply_nodal_block8 (topovox/backends/numba_kernels.py:61-76; seam
+ * topovox/backends/__init__.py:52): d_out += sum_e P_e^T (B_e (x) I3) P_e d_u
+ * with d_blocks f64[Ne][8][8] in the element's local (VTK) node order. */
+int tvb_nodal_block8(int nx, int ny, int nz, const double* d_u, double* d_out, const double* d_blocks, void* stream);
+/* geometric stiffness K_G u with B_e = sum_k stress[e][k] * Bk[k] (Bk = the
+ * 6 Voigt components of geometric_tensor, elements.py:141-153, device
+ * f64[6][8][8]); flags: 1 zero fixed DOFs of u, 2 zero fixed rows of the
+ * output, 4 accumulate; output scaled by `scale`. */
+int tvb_geo_matvec(int nx, int ny, int nz, const double* d_Bk, const double* d_stress, const double* d_u,
+                   double* d_out, const uint8_t* d_nflags, int flags, double scale, void* stream);
+/* MassOperator: d_mass f64[3*Nn] = coef * sum of the
+ * occupancies of the node's elements, coef = rho h^3 / 8. */
+int tvb_lumped_mass(int nx, int ny, int nz, double coef, const double* d_occ, double* d_mass, void* stream);
+/* eigen_sensitivity T_lambda = sigma(u):eps(u) - omega2rho * occ_e * |u(centroid)|^2
+ * (omega2rho = omega_n^2 rho). */
+int tvb_eigen_sens(int nx, int ny, int nz, double h, double E, double nu, const double* d_u, const double* d_occ,
+                   double omega2rho, double* d_out, void* stream);
+/* buckling_sensitivity T_p = u_e^T K^e u_e - lambda u_e^T K_sigma^e u_e with
+ * K^e = occ_e k0 (d_k0 device f64[24][24]) and K_sigma = -K_G (compression
+ * positive): = occ_e u_e^T k0 u_e + lambda sum_a u_ea^T B_e u_ea. */
+int tvb_buckling_sens(int nx, int ny, int nz, const double* d_k0, const double* d_Bk, const double* d_stress,
+                      const double* d_u, const double* d_occ, double lambda, double* d_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -420,6 +420,124 @@ def stress_adjoint_rhs(op: Operator, u, p):
     return rhs
 
 
+# ---------------------------------------------------------------------------
+# eigen / buckling -- dense, small
+# problems only (<= a few thousand DOFs)
+# ---------------------------------------------------------------------------
+def geometric_tensor(h):
+    """topovox/elements.py:141-153: A[p,q,i,j] = sum_gp dNi/dx_p dNj/dx_q detJ."""
+    A = np.zeros((3, 3, 8, 8))
+    a = 1.0 / np.sqrt(3.0)
+    for gp in a * (2.0 * OFFS - 1.0):
+        dn = _dshape(*gp) * (2.0 / h)
+        A += np.einsum("ip,jq->pqij", dn, dn) * (h / 2.0) ** 3
+    return A
+
+
+def voigt_tensor(s):
+    """(..., 6) Voigt (xx, yy, zz, xy, yz, zx) -> (..., 3, 3)."""
+    s = np.asarray(s)
+    t = np.empty(s.shape[:-1] + (3, 3))
+    t[..., 0, 0], t[..., 1, 1], t[..., 2, 2] = s[..., 0], s[..., 1], s[..., 2]
+    t[..., 0, 1] = t[..., 1, 0] = s[..., 3]
+    t[..., 1, 2] = t[..., 2, 1] = s[..., 4]
+    t[..., 2, 0] = t[..., 0, 2] = s[..., 5]
+    return t
+
+
+def stress_blocks(stresses, h):
+    """Per-element 8x8 initial-stress blocks sum_pq sigma_pq A[p,q]."""
+    return np.einsum("epq,pqij->eij", voigt_tensor(stresses), geometric_tensor(h))
+
+
+def apply_nodal_block8(op: Operator, u, blocks):
+    """topovox/backends/numpy_kernels.py:26-30 (numba_kernels.py:61-76):
+    sum_e P_e^T (B_e (x) I3) P_e u, unmasked."""
+    dofs = op.edofs.reshape(-1, 8, 3)
+    fe = np.einsum("eij,eja->eia", blocks, np.asarray(u)[dofs])
+    out = np.zeros(op.n_dofs)
+    np.add.at(out, dofs, fe)
+    return out
+
+
+def dense_geometric(op: Operator, stresses):
+    """Assembled K_G (raw) from the element stresses."""
+    blocks = stress_blocks(stresses, op.h)
+    K = np.zeros((op.n_dofs, op.n_dofs))
+    for e in range(op.occ.size):
+        d = op.edofs[e].reshape(8, 3)
+        for a in range(3):
+            K[np.ix_(d[:, a], d[:, a])] += blocks[e]
+    return K
+
+
+def lumped_mass(op: Operator, rho):
+    """rho h^3 / 8 occupancy_e to each corner, per DOF."""
+    m = np.zeros(op.n_dofs)
+    np.add.at(m, op.edofs, np.repeat(rho * op.h ** 3 / 8.0 * op.occ[:, None], 24, axis=1))
+    return m
+
+
+def dense_modal(op: Operator, rho, k):
+    """k smallest eigenpairs of K u = lambda M u on the free DOFs (scipy eigh)."""
+    import scipy.linalg
+
+    f = op.free
+    K = dense_stiffness(op)[np.ix_(f, f)]
+    M = lumped_mass(op, rho)[f]
+    w, V = scipy.linalg.eigh(K, np.diag(M))
+    U = np.zeros((op.n_dofs, k))
+    U[f] = V[:, :k]
+    return w[:k], U
+
+
+def buckling_cap(strains, frac=0.1):
+    """Search cap of the load factor ("below a search cap"): the
+    factor at which the largest reference strain component reaches `frac`
+    (10 %), far outside linear buckling theory (builder decision)."""
+    m = float(np.abs(strains).max()) if np.size(strains) else 0.0
+    return frac / m if m > 0.0 else np.inf
+
+
+def dense_buckling(op: Operator, stresses, k, cap=np.inf):
+    """k smallest positive lambda <= cap of K phi = lambda K_sigma phi,
+    K_sigma = -K_G, on the free DOFs: via K^-1 K_sigma's largest
+    positive mu."""
+    import scipy.linalg
+
+    f = op.free
+    K = dense_stiffness(op)[np.ix_(f, f)]
+    Ks = -dense_geometric(op, stresses)[np.ix_(f, f)]
+    mu, V = scipy.linalg.eigh(Ks, K)  # Ks v = mu K v, mu = 1 / lambda
+    order = np.argsort(-mu)
+    mu, V = mu[order], V[:, order]
+    pos = (mu > 1e-8 * np.abs(mu).max()) & (mu >= 1.0 / cap)
+    lam = 1.0 / mu[pos][:k]
+    U = np.zeros((op.n_dofs, lam.size))
+    U[f] = V[:, pos][:, :k]
+    return lam, U
+
+
+def eigen_sensitivity(op: Operator, mode, omega2, rho):
+    """T_lambda = sigma(u):eps(u) - omega^2 rho_e |u_centroid|^2,
+    rho_e = rho occupancy_e (the mass operator's density)."""
+    strains, stresses, _ = batch_element_state(op, mode)
+    se = np.einsum("ij,ij->i", stresses, strains)
+    uc = np.asarray(mode)[op.edofs].reshape(-1, 8, 3).mean(axis=1)
+    return se - omega2 * rho * op.occ * np.einsum("ij,ij->i", uc, uc)
+
+
+def buckling_sensitivity(op: Operator, stresses, mode, lam):
+    """T_p = u_e^T K^e u_e - lambda u_e^T K_sigma^e u_e with
+    K^e = occ_e k0 and K_sigma^e = -(B_e (x) I3)."""
+    ue = np.asarray(mode)[op.edofs]  # (ne, 24)
+    e1 = op.occ * np.einsum("ei,ij,ej->e", ue, op.k0, ue)
+    blocks = stress_blocks(stresses, op.h)
+    u3 = ue.reshape(-1, 8, 3)
+    e2 = np.einsum("eia,eij,eja->e", u3, blocks, u3)
+    return e1 + lam * e2
+
+
 def normalize_field(t):
     """SPEC.md:378"""
     t = np.asarray(t, dtype=float)

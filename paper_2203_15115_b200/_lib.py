@@ -92,6 +92,11 @@ _SIGS = {
     "tvb_threshold_select": (c_int, [P, P, c_ll, c_ll, c_double, c_double, P, P, c_size_t, P, P]),
     "tvb_threshold_select_ex": (c_int, [P, P, c_ll, c_ll, c_double, c_double, c_int, P, P, c_size_t, P, P]),
     "tvb_casting_project": (c_int, [c_int, c_int, c_int, c_int, c_int, P, P, P]),
+    "tvb_nodal_block8": (c_int, [c_int, c_int, c_int, P, P, P, P]),
+    "tvb_geo_matvec": (c_int, [c_int, c_int, c_int, P, P, P, P, P, c_int, c_double, P]),
+    "tvb_lumped_mass": (c_int, [c_int, c_int, c_int, c_double, P, P, P]),
+    "tvb_eigen_sens": (c_int, [c_int, c_int, c_int, c_double, c_double, c_double, P, P, c_double, P, P]),
+    "tvb_buckling_sens": (c_int, [c_int, c_int, c_int, P, P, P, P, P, c_double, P, P]),
 }
 
 MASK_IN, MASK_OUT, ACCUMULATE = 1, 2, 4

@@ -110,6 +110,21 @@ def diag_block24(out, elem_dofs, scale, k0_diag):
     _writeback(out, out_d)
 
 
+def apply_nodal_block8(u, out, elem_dofs, blocks, color_perm=None, color_ptr=None):
+    """out += scatter of per-element 8x8 nodal blocks acting on each
+    displacement component (reference ``numba_kernels.py:61-76``; geometric
+    stiffness). blocks: (Ne, 8, 8) in the element's local node order."""
+    torch = require_cuda()
+    dims = grid_from_elem_dofs(elem_dofs)
+    _check_table(elem_dofs, dims)
+    ne = dims[0] * dims[1] * dims[2]
+    if tuple(blocks.shape) != (ne, 8, 8):
+        raise DimensionMismatch(f"blocks have shape {tuple(blocks.shape)}, expected ({ne}, 8, 8)")
+    u_d, out_d, b_d = _dev(u, torch.float64), _dev(out, torch.float64), _dev(blocks, torch.float64)
+    check(lib().tvb_nodal_block8(*dims, ptr(u_d), ptr(out_d), ptr(b_d), stream_ptr()), "apply_nodal_block8")
+    _writeback(out, out_d)
+
+
 def element_coloring(ix, iy, iz):
     """Parity colouring (reference ``backends/__init__.py:59-66``); kept for
     API compatibility -- the CUDA kernels do not need it."""

@@ -9,6 +9,7 @@
 #include "../../include/topovox_b200.h"
 #include "coarse.cuh"
 #include "deflation.cuh"
+#include "eigen.cuh"
 #include "fields.cuh"
 #include "matvec.cuh"
 #include "solver.cuh"
@@ -704,6 +705,55 @@ int tvb_casting_project(int nx, int ny, int nz, int axis, int parting, const dou
   const int na = axis == 0 ? nx : axis == 1 ? ny : nz;
   if (parting < 0 || parting > na) return kStatusBadArg;
   return check(launch_casting_project(G, axis, parting, d_in, d_out, (cudaStream_t)stream));
+}
+
+/* ---- eigen / buckling ---------------------------------------- */
+int tvb_nodal_block8(int nx, int ny, int nz, const double* d_u, double* d_out, const double* d_blocks, void* stream) {
+  if (bad_dims(nx, ny, nz) || !d_u || !d_out || !d_blocks) return kStatusBadArg;
+  GeoArgs A{};
+  A.g = make_grid(nx, ny, nz);
+  A.u = d_u;
+  A.y = d_out;
+  A.blocks = d_blocks;
+  A.accumulate = 1;  // apply_nodal_block8 accumulates into out
+  A.scale = 1.0;
+  return check(launch_geo_matvec(A, (cudaStream_t)stream));
+}
+
+int tvb_geo_matvec(int nx, int ny, int nz, const double* d_Bk, const double* d_stress, const double* d_u,
+                   double* d_out, const uint8_t* d_nflags, int flags, double scale, void* stream) {
+  if (bad_dims(nx, ny, nz) || !d_Bk || !d_stress || !d_u || !d_out) return kStatusBadArg;
+  GeoArgs A{};
+  A.g = make_grid(nx, ny, nz);
+  A.u = d_u;
+  A.y = d_out;
+  A.stress = d_stress;
+  A.Bk = d_Bk;
+  A.nflags = d_nflags;
+  A.mask_in = (flags & 1) != 0;
+  A.mask_out = (flags & 2) != 0;
+  A.accumulate = (flags & 4) != 0;
+  A.scale = scale;
+  return check(launch_geo_matvec(A, (cudaStream_t)stream));
+}
+
+int tvb_lumped_mass(int nx, int ny, int nz, double coef, const double* d_occ, double* d_mass, void* stream) {
+  if (bad_dims(nx, ny, nz) || !d_occ || !d_mass) return kStatusBadArg;
+  return check(launch_lumped_mass(make_grid(nx, ny, nz), coef, d_occ, d_mass, (cudaStream_t)stream));
+}
+
+int tvb_eigen_sens(int nx, int ny, int nz, double h, double E, double nu, const double* d_u, const double* d_occ,
+                   double omega2rho, double* d_out, void* stream) {
+  if (bad_dims(nx, ny, nz) || !d_u || !d_occ || !d_out || !(h > 0.0)) return kStatusBadArg;
+  const ElemArgs A = elem_args(nx, ny, nz, h, E, nu, d_u, d_occ);
+  return check(launch_eigen_sens(A, omega2rho, d_out, (cudaStream_t)stream));
+}
+
+int tvb_buckling_sens(int nx, int ny, int nz, const double* d_k0, const double* d_Bk, const double* d_stress,
+                      const double* d_u, const double* d_occ, double lambda, double* d_out, void* stream) {
+  if (bad_dims(nx, ny, nz) || !d_k0 || !d_Bk || !d_stress || !d_u || !d_occ || !d_out) return kStatusBadArg;
+  return check(launch_buckling_sens(make_grid(nx, ny, nz), d_k0, d_Bk, d_stress, d_u, d_occ, lambda, d_out,
+                                    (cudaStream_t)stream));
 }
 
 }  // extern "C"

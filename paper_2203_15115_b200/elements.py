@@ -111,6 +111,38 @@ def hex_stiffness(material: Material, h: float) -> np.ndarray:
     return 0.5 * (k + k.T)
 
 
+def geometric_tensor(h: float) -> np.ndarray:
+    """A[p, q, i, j] = sum_gp dNi/dx_p dNj/dx_q detJ over the 2x2x2 rule
+    (reference ``topovox/elements.py:141-153``): contracting a constant stress
+    tensor against (p, q) gives the 8x8 nodal block of the initial-stress
+    matrix (replicated on each displacement component)."""
+    if not h > 0.0:
+        raise ValueError(f"edge length must be positive, got {h}")
+    jac = (0.5 * h) ** 3
+    g = 1.0 / np.sqrt(3.0)
+    A = np.zeros((3, 3, 8, 8))
+    for sx in (-1.0, 1.0):
+        for sy in (-1.0, 1.0):
+            for sz in (-1.0, 1.0):
+                dn = _grad_ref((sx * g, sy * g, sz * g)) * (2.0 / h)  # (8, 3)
+                A += jac * np.einsum("ip,jq->pqij", dn, dn)
+    return A
+
+
+#: Voigt component order of element stresses (xx, yy, zz, xy, yz, zx)
+_VOIGT_PQ = ((0, 0), (1, 1), (2, 2), (0, 1), (1, 2), (2, 0))
+
+
+def geometric_voigt_blocks(h: float) -> np.ndarray:
+    """(6, 8, 8) blocks Bk with sum_pq sigma_pq A[p, q] = sum_k s_k Bk[k] for a
+    Voigt stress row s (off-diagonal components enter A[p,q] + A[q,p])."""
+    A = geometric_tensor(h)
+    out = np.empty((6, 8, 8))
+    for k, (p, q) in enumerate(_VOIGT_PQ):
+        out[k] = A[p, q] if p == q else A[p, q] + A[q, p]
+    return out
+
+
 def centroid_b_matrix(h: float) -> np.ndarray:
     """B evaluated at the element centroid (reference ``elements.py:135-138``)."""
     return strain_displacement(_grad_ref((0.0, 0.0, 0.0)) * (2.0 / h))

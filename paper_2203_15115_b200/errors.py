@@ -61,6 +61,17 @@ class ConfigRejected(SemanticError):
     """Constraint set-up that would stop the optimizer at its first step."""
 
 
+class NoPositiveFactor(TopovoxError):
+    """Buckling: no positive load factor below the search cap (structure in
+    pure tension). solve_buckling reports it as the P = +inf
+    sentinel instead of raising; the class names the outcome."""
+
+
+class ZeroMassSubspace(UserWarning):
+    """Modal analysis: free DOFs with zero lumped mass; they
+    are reported and excluded from the eigen subspace."""
+
+
 class CudaError(TopovoxError):
     """The CUDA runtime reported an error inside the native library."""
 

@@ -148,3 +148,62 @@ def test_spec_casting_kats(oracle):
     # monotone columns are unchanged
     mono = np.repeat(np.arange(6, 0, -1, dtype=float), 35).reshape(6, 5, 7).reshape(-1)
     assert np.array_equal(oracle.casting_project(mono, dims, 2, 0), mono)
+
+
+def test_geometric_tensor_and_nodal_block8_vs_reference(oracle):
+    """The oracle's geometric_tensor / apply_nodal_block8 restatements against
+    the REAL reference (tests/golden/make_golden_geo.py)."""
+    import os
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_golden_geo.npz"))
+    assert np.abs(oracle.geometric_tensor(1.0) - g["A_h1"]).max() <= 1e-15
+    assert np.abs(oracle.geometric_tensor(0.5) - g["A_h05"]).max() <= 1e-15 * np.abs(g["A_h05"]).max()
+    for name in ("g543", "g217"):
+        dims, h = tuple(int(v) for v in g[f"{name}_dims"]), float(g[f"{name}_h"])
+        op = oracle.Operator(*dims, h, g[f"{name}_occ"])
+        _, st, _ = oracle.batch_element_state(op, g[f"{name}_w"])
+        assert np.abs(st - g[f"{name}_stress"]).max() <= 1e-14 * np.abs(st).max()
+        kg = oracle.apply_nodal_block8(op, g[f"{name}_u"], oracle.stress_blocks(g[f"{name}_stress"], h))
+        assert np.abs(kg - g[f"{name}_KGu"]).max() <= 1e-13 * np.abs(g[f"{name}_KGu"]).max()
+        bu = oracle.apply_nodal_block8(op, g[f"{name}_u"], g[f"{name}_blocks"])
+        assert np.abs(bu - g[f"{name}_Bu"]).max() <= 1e-13 * np.abs(g[f"{name}_Bu"]).max()
+
+
+def test_spec_eigen_kats(oracle):
+    """SPEC.md:226-227, 245-247, 324-335 on the dense oracle."""
+    # free-free single element: six rigid modes, |lambda| / lambda_7 <= 1e-6
+    op = oracle.Operator(1, 1, 1, 1.0, np.ones(1))
+    w, _ = oracle.dense_modal(op, 1.0, 7)
+    assert np.all(np.abs(w[:6]) <= 1e-6 * w[6])
+    # density scaling rho -> c rho scales eigenvalues by 1/c
+    op = oracle.Operator(4, 2, 2, 1.0, np.ones(16), dirichlet=np.arange(3 * 15))
+    w1, _ = oracle.dense_modal(op, 1.0, 3)
+    w4, _ = oracle.dense_modal(op, 4.0, 3)
+    assert np.allclose(w4, w1 / 4.0, rtol=1e-12)
+    # T_lambda direct substitution and rigid mode -> 0
+    u = np.tile([0.3, -0.2, 0.5], op.n_dofs // 3)
+    assert np.abs(oracle.eigen_sensitivity(op, u, 0.0, 1.0)).max() <= 1e-15
+    # T_p sums to u^T (K - lambda K_sigma) u and vanishes at a buckling pair
+    col = oracle.Operator(2, 2, 8, 1.0, np.ones(32), dirichlet=np.arange(27))
+    f = np.zeros(col.n_dofs)
+    top = [3 * (x + 3 * (y + 3 * 8)) + 2 for x in range(3) for y in range(3)]
+    f[top] = -1.0 / 9
+    import scipy.linalg
+
+    Kf = oracle.dense_stiffness(col)[np.ix_(col.free, col.free)]
+    uref = np.zeros(col.n_dofs)
+    uref[col.free] = scipy.linalg.solve(Kf, f[col.free])
+    sn, st, _ = oracle.batch_element_state(col, uref)
+    cap = oracle.buckling_cap(sn)
+    lam, U = oracle.dense_buckling(col, st, 1, cap)
+    tp = oracle.buckling_sensitivity(col, st, U[:, 0], lam[0])
+    ktot = U[:, 0] @ oracle.dense_stiffness(col) @ U[:, 0]
+    assert abs(tp.sum()) <= 1e-8 * ktot
+    # halving the load doubles P; tension has no positive factor
+    lam2, _ = oracle.dense_buckling(col, 0.5 * st, 1, oracle.buckling_cap(0.5 * sn))
+    assert lam2[0] == pytest.approx(2 * lam[0], rel=1e-10)
+    # pure tension: only local factors far beyond the search cap (27.8 vs cap ~ 0.3)
+    lamt, _ = oracle.dense_buckling(col, -st, 1, cap)
+    assert lamt.size == 0
+    # Euler: P within 15 % of pi^2 E I / (4 L^2) / F on the 2x2x8 column
+    assert lam[0] == pytest.approx(np.pi ** 2 * (2 ** 4 / 12) / (4 * 64), rel=0.15)
