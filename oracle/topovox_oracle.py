@@ -634,8 +634,10 @@ def update_penalty(gamma, g_prev, g_new, k, varsigma=0.25, eta=10.0):
 # independently for whole-run checks on small grids. Constraints: compliance
 # and p-norm stress per load case (the SPEC kinds used by the configs).
 # ---------------------------------------------------------------------------
-def _analyses(nx, ny, nz, occ, cases, specs, E, nu, tol, block, need_fields=True):
-    """cases: list of (fixed_dofs, f); specs: list of dicts(kind, alpha, soft, case, p)."""
+def _analyses(nx, ny, nz, occ, cases, specs, E, nu, tol, block, need_fields=True, rho=1.0):
+    """cases: list of (fixed_dofs, f); specs: list of dicts(kind, alpha, soft,
+    case, p[, sense]). Eigenvalue / buckling kinds use the dense eigen
+    oracles (small problems only)."""
     out = {"q": {}, "fields": {}, "J": 0.0}
     for ci, (fixed, f) in enumerate(cases):
         op = Operator(nx, ny, nz, 1.0, occ, E=E, nu=nu, dirichlet=fixed)
@@ -656,20 +658,43 @@ def _analyses(nx, ny, nz, occ, cases, specs, E, nu, tol, block, need_fields=True
                     lam, _, _ = solve_static(op, stress_adjoint_rhs(op, u, s["p"]), tol=tol, deflation=defl)
                     ls, _, _ = batch_element_state(op, lam)
                     out["fields"][i] = stress_sensitivity(stresses, ls, nu)
+            elif s["kind"] == "eigenvalue":
+                w, U = dense_modal(op, rho, 1)
+                out["q"][i] = float(w[0])
+                out["fields"][i] = eigen_sensitivity(op, U[:, 0], w[0], rho)
+            elif s["kind"] == "buckling":
+                lam, U = dense_buckling(op, stresses, 1, buckling_cap(strains))
+                if lam.size == 0:
+                    out["q"][i] = np.inf
+                    out["fields"][i] = np.zeros(op.occ.size)
+                else:
+                    phi = U[:, 0] / np.linalg.norm(U[:, 0].reshape(-1, 3), axis=1).max()
+                    out["q"][i] = float(lam[0])
+                    out["fields"][i] = buckling_sensitivity(op, stresses, phi, lam[0])
     return out
+
+
+def constraint_value(q, q0, alpha, sense):
+    """SPEC.md:469 with the +inf sentinel rule of the device driver."""
+    if np.isinf(q) or np.isinf(q0):
+        if (sense == "lower" and q > 0) or np.isinf(q0):
+            return -1.0
+    return constraint_g(q, q0, alpha, sense)
 
 
 def run_optimizer(nx, ny, nz, cases, specs, E=1.0, nu=0.3, tol=1e-8, block=4, ersatz=1e-6, mu0=100.0, gamma0=10.0,
                   varsigma=0.25, eta=10.0, dv0=0.025, dv_min=0.005, growth=1.1, growth_after=3, inner_cap=10,
-                  ctol=0.01, ttol=0.001, feas=1e-6, max_outer=400, casting=None):
+                  ctol=0.01, ttol=0.001, feas=1e-6, max_outer=400, casting=None, rho=1.0):
     """Returns (occ, history list of dicts, reason). casting: (axis, parting
     element layer) -> casting-projected extraction with all ties retained."""
     ne = nx * ny * nz
     design = np.ones(ne, dtype=bool)
     occ = np.ones(ne)
-    base = _analyses(nx, ny, nz, occ, cases, specs, E, nu, tol, block)
+    base = _analyses(nx, ny, nz, occ, cases, specs, E, nu, tol, block, rho=rho)
     q0 = dict(base["q"])
-    gfun = lambda q: {i: constraint_g(q[i], q0[i], s["alpha"], "upper") for i, s in enumerate(specs)}  # noqa: E731
+    sense = [s.get("sense", "lower" if s["kind"] in ("eigenvalue", "buckling") else "upper") for s in specs]
+    gfun = lambda q: {i: constraint_value(q[i], q0[i], s["alpha"], sense[i])  # noqa: E731
+                      for i, s in enumerate(specs)}
     g = gfun(base["q"])
     mu = {i: mu0 for i in range(len(specs))}
     gam = {i: gamma0 for i in range(len(specs))}
@@ -695,7 +720,7 @@ def run_optimizer(nx, ny, nz, cases, specs, E=1.0, nu=0.3, tol=1e-8, block=4, er
             if it > 1 and np.count_nonzero((new_occ == 1.0) != (cur_occ == 1.0)) < ttol * ne:
                 conv = True
                 break
-            nxt = _analyses(nx, ny, nz, new_occ, cases, specs, E, nu, tol, block)
+            nxt = _analyses(nx, ny, nz, new_occ, cases, specs, E, nu, tol, block, rho=rho)
             if it > 1 and abs(nxt["J"] - cur["J"]) < ctol * cur["J"]:
                 cur, cur_occ, conv = nxt, new_occ, True
                 break

@@ -158,17 +158,31 @@ def geometric_stiffness(u_ref, op: StiffnessOperator) -> GeometricStiffnessOpera
 # ---------------------------------------------------------------------------
 # shift-invert subspace iteration
 # ---------------------------------------------------------------------------
+def _inner_tol(tol: float) -> float:
+    """Inner (deflated-CG) tolerance for an eigen residual target `tol`."""
+    return min(1e-8, max(1e-13, 1e-2 * tol))
+
+
+def _inner_iters(op) -> int:
+    """Generous inner cap: low-volume ersatz topologies stagnate slowly."""
+    from .fea import default_max_iters
+
+    return 4 * default_max_iters(op.n_dofs)
+
+
 def _inner_solver(op, deflation, shift, mass, inner_tol):
     """X -> (K + shift M)^-1 X column batch on the device."""
     torch = _t()
     if shift == 0.0:
-        return lambda cols: [r.u for r in solve_static_batch(op, cols, tol=inner_tol, deflation=deflation)]
+        return lambda cols: [r.u for r in solve_static_batch(op, cols, tol=inner_tol, deflation=deflation,
+                                                             max_iters=_inner_iters(op))]
     kd = op.diagonal_device() + shift * mass.diag_d
 
     def apply(v):
         return op.apply_device(v) + shift * mass.diag_d * v
 
-    return lambda cols: [solve_static(op, c, tol=inner_tol, apply_op=apply, diag=kd).u for c in cols]
+    return lambda cols: [solve_static(op, c, tol=inner_tol, apply_op=apply, diag=kd, max_iters=_inner_iters(op)).u
+                         for c in cols]
 
 
 def _rayleigh_ritz(A, B):
@@ -222,7 +236,7 @@ def solve_modal(op: StiffnessOperator, mass: MassOperator, k: int = 1, tol: floa
         else:  # free-free: K singular (rigid modes); shift by ~1e-2 of the mean diagonal ratio
             kd = op.diagonal_device()
             shift = 1e-2 * float((kd[active] / m[active]).mean())
-    inner_tol = inner_tol if inner_tol is not None else min(1e-10, 1e-3 * tol)
+    inner_tol = inner_tol if inner_tol is not None else _inner_tol(tol)
     solve = _inner_solver(op, deflation, shift, mass, inner_tol)
     X = _start_block(n, q, active, seed)
     w = None
@@ -277,7 +291,7 @@ def solve_buckling(op: StiffnessOperator, geo: GeometricStiffnessOperator, k: in
     free = torch.from_numpy(op.free_mask).cuda()
     n_free = int(free.sum())
     q = min(subspace or max(2 * k, k + 7), n_free)
-    inner_tol = inner_tol if inner_tol is not None else min(1e-10, 1e-3 * tol)
+    inner_tol = inner_tol if inner_tol is not None else _inner_tol(tol)
     cap = geo.search_cap() if lambda_cap is None else float(lambda_cap)
     mu_min = 1.0 / cap if cap > 0.0 else math.inf
     X = _start_block(n, q, free, seed)
@@ -290,7 +304,7 @@ def solve_buckling(op: StiffnessOperator, geo: GeometricStiffnessOperator, k: in
         if not bool(Y.any()):
             return inf_result(it)  # zero stress state: K_sigma = 0
         cols = [r.u for r in solve_static_batch(op, [Y[:, j].contiguous() for j in range(q)], tol=inner_tol,
-                                                deflation=deflation)]
+                                                deflation=deflation, max_iters=_inner_iters(op))]
         solves += q
         Xb = torch.stack(cols, dim=1)
         B = Xb.T @ Y                       # Xb^T K Xb

@@ -20,7 +20,11 @@ Builder decisions (documented in DESIGN.md §6):
     not in the SPEC's list; they are evaluated as |u_dof| and their field is
     the mutual-energy form 4/(1+nu) s(u):e(l) - (1-3nu)/(1-nu^2) tr s tr e with
     K l = e_dof (the same topological-derivative form as Eq 3.3);
-  * p-norm constraints use the p of their ConstraintSpec (C4/C5: p = 8).
+  * p-norm constraints use the p of their ConstraintSpec (C4/C5: p = 8);
+  * eigenvalue / buckling constraints (lower sense by default)
+    run eigen.solve_modal / eigen.solve_buckling on the constrained case's
+    operator; their fields are T_lambda / T_p; a buckling
+    factor reported as the +inf sentinel gives g = -1.
 """
 
 from __future__ import annotations
@@ -46,18 +50,21 @@ class ConstraintSpec:
 
     kind: str
     alpha: float
-    sense: str = "upper"
+    sense: str | None = None  # default: upper for compliance/stress/displacement, lower for eigenvalue/buckling
     soft: bool = False
     load_case: str = ""
     p: int = 6
     dof: int | None = None
     override: bool = False
+    modes: int = 1            # eigenpairs computed for an eigenvalue constraint (the lowest is constrained)
 
     def __post_init__(self):
         if self.kind not in KINDS:
             raise SemanticError(f"unknown constraint kind {self.kind!r}")
-        if self.kind in ("eigenvalue", "buckling"):
-            raise NotImplementedError("eigenvalue/buckling analyses are outside the B200 hot path (SURVEY §8f)")
+        if self.sense is None:  # eigenvalue/buckling are lower-sense
+            object.__setattr__(self, "sense", "lower" if self.kind in ("eigenvalue", "buckling") else "upper")
+        if self.modes < 1:
+            raise SemanticError("modes must be >= 1")
         if self.sense not in ("upper", "lower"):
             raise SemanticError(f"sense must be upper|lower, got {self.sense!r}")
         if self.sense == "lower" and not self.soft and self.alpha >= 1.0 and not self.override:
@@ -85,6 +92,7 @@ class OptimizerConfig:
     feas_tol: float = 1e-6
     ersatz: float = EPS_VOID
     tol: float = 1e-8
+    eigen_tol: float = 1e-6
     block: int = 4
     max_outer: int = 400
     min_volume: float = 0.0
@@ -120,6 +128,14 @@ class IterationRecord:
 # scalar machinery
 # ---------------------------------------------------------------------------
 def constraint_value(q: float, q0: float, alpha: float, sense: str) -> float:
+    """SPEC.md:469. A buckling factor reported as the +inf sentinel (no
+    positive factor) satisfies a lower bound: g = -1 (builder
+    decision); so does any constraint whose baseline q0 is +inf (vacuous)."""
+    if math.isinf(q) or math.isinf(q0):
+        if sense == "lower" and q > 0.0:
+            return -1.0
+        if math.isinf(q0):
+            return -1.0
     return q / (alpha * q0) - 1.0 if sense == "upper" else 1.0 - q / (alpha * q0)
 
 
@@ -226,12 +242,45 @@ class Analyses:
                             e = torch.zeros_like(u)
                             e[spec.dof] = math.copysign(1.0, float(u[spec.dof]))
                             adjoints.append((name, u, e))
+            self._eigen_analyses(problem, specs, cfg, op, defl, members, sols, need_fields)
             if adjoints:
                 lams = fea.solve_static_batch(op, [rhs for _, _, rhs in adjoints], tol=cfg.tol, deflation=defl)
                 self.solves += len(adjoints)
                 for (name, u, _), lam in zip(adjoints, lams):
                     self.fields[name] = sensitivity.stress_sensitivity(op, u, lam.u)
         self.J_total = float(sum(self.J.values()))
+
+    def _eigen_analyses(self, problem, specs, cfg, op, defl, members, sols, need_fields):
+        """Modal and buckling analyses of
+        the constraints attached to this Dirichlet group; only run when a
+        constraint asks for them."""
+        from . import eigen
+
+        torch = __import__("torch")
+        ids = {case.id: i for i, (case, _) in enumerate(members)}
+        modal = None
+        for name, spec in specs.items():
+            cid = spec.load_case or problem.load_cases[0].id
+            if cid not in ids:
+                continue
+            if spec.kind == "eigenvalue":
+                if modal is None or len(modal.values) < spec.modes:
+                    modal = eigen.solve_modal(op, eigen.MassOperator(op), k=spec.modes, tol=cfg.eigen_tol,
+                                              deflation=defl)
+                    self.solves += modal.solves
+                self.q[name] = float(modal.values[0])
+                if need_fields:
+                    self.fields[name] = eigen.eigen_sensitivity(op, modal.vectors[0], modal.values[0])
+            elif spec.kind == "buckling":
+                u = sols[ids[cid]].u
+                geo = eigen.geometric_stiffness(u, op)
+                r = eigen.solve_buckling(op, geo, k=1, tol=cfg.eigen_tol, deflation=defl)
+                self.solves += r.solves
+                self.q[name] = float(r.values[0])
+                if need_fields:
+                    self.fields[name] = (torch.zeros(op.domain.n_elems, dtype=torch.float64, device="cuda")
+                                         if r.no_positive_factor else
+                                         eigen.buckling_sensitivity(op, geo, r.vectors[0], r.values[0]))
 
 
 def _compliance_fallback(specs: dict) -> str:

@@ -32,8 +32,16 @@ def test_config_validation():
     with pytest.raises(ConfigRejected):
         opt.ConstraintSpec("compliance", 1.2, sense="lower")
     opt.ConstraintSpec("compliance", 1.5, sense="lower", soft=True)  # soft lower alpha>1 is legal
-    with pytest.raises(NotImplementedError):
-        opt.ConstraintSpec("buckling", 0.5, sense="lower")
+    # eigenvalue / buckling default to lower sense; hard alpha >= 1 rejected
+    assert opt.ConstraintSpec("buckling", 0.5).sense == "lower"
+    assert opt.ConstraintSpec("eigenvalue", 0.8).sense == "lower"
+    with pytest.raises(ConfigRejected):
+        opt.ConstraintSpec("eigenvalue", 1.2)
+    opt.ConstraintSpec("buckling", 1.2, soft=True)  # PAPER Table 4 scenario 3: soft alpha > 1 legal
+    # the +inf buckling sentinel satisfies a lower bound; a vacuous baseline too
+    assert opt.constraint_value(float("inf"), 2.0, 0.5, "lower") == -1.0
+    assert opt.constraint_value(3.0, float("inf"), 0.5, "lower") == -1.0
+    assert opt.constraint_value(0.16, 1.0, 0.1, "lower") == pytest.approx(-0.6)
     with pytest.raises(MissingAnalysis):
         opt.evaluate_constraints({"a": opt.ConstraintSpec("compliance", 2.0)}, {}, {})
 
@@ -102,3 +110,73 @@ def test_whole_run_small_cantilever(oracle):
     assert abs(topo.volume_fraction - float(np.mean(occ_r == 1.0))) <= 0.05
     # hard constraint satisfied at the accepted design
     assert all(g <= 1e-6 for h in hist if h.accepted for g in h.g.values())
+
+
+def _column_problem(n=2, L=8, rho=1.0):
+    from paper_2203_15115_b200.elements import Material
+    from paper_2203_15115_b200.mesh import Domain, LoadCase, RegionSelector
+
+    d = Domain(n, n, L, 1.0)
+    case = LoadCase("col", dirichlet=((RegionSelector("box", min=(0, 0, 0), max=(n, n, 0)), (1, 1, 1)),),
+                    loads=((RegionSelector("box", min=(0, 0, L), max=(n, n, L)), (0, 0, -1), "total"),))
+    return d, case, Material(E=1.0, nu=0.3, rho=rho)
+
+
+@pytest.mark.gpu
+def test_eigen_buckling_analyses_resynced(oracle):
+    """Eigenvalue (T_lambda) and buckling (T_p) constraints on one topology:
+    device q and fields against the dense oracle."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2203_15115_b200.mesh import Topology, assemble_force, dirichlet_dofs
+
+    d, case, mat = _column_problem(2, 8)
+    prob = opt.Problem(d, mat, [case], [opt.ConstraintSpec("compliance", 2.0),
+                                        opt.ConstraintSpec("eigenvalue", 0.5),
+                                        opt.ConstraintSpec("buckling", 0.5)])
+    cfg = opt.OptimizerConfig(ersatz=1e-3, block=2, tol=1e-12, eigen_tol=1e-10)
+    specs = {f"c{i}": c for i, c in enumerate(prob.constraints)}
+    assert specs["c1"].sense == "lower" and specs["c2"].sense == "lower" and specs["c0"].sense == "upper"
+    occ = np.where(np.random.default_rng(4).random(d.n_elems) < 0.85, 1.0, 1e-3)
+    an = opt.Analyses(prob, specs, Topology(d, occ), cfg)
+    fixed, f = dirichlet_dofs(d, case), assemble_force(d, case)
+    ref = oracle._analyses(2, 2, 8, occ, [(fixed, f)],
+                           [{"kind": "compliance", "alpha": 2.0, "case": 0},
+                            {"kind": "eigenvalue", "alpha": 0.5, "case": 0},
+                            {"kind": "buckling", "alpha": 0.5, "case": 0}], 1.0, 0.3, 1e-12, 2)
+    for i, name in enumerate(specs):
+        assert an.q[name] == pytest.approx(ref["q"][i], rel=1e-8), name
+        got = an.fields[name].cpu().numpy()
+        assert np.abs(got - ref["fields"][i]).max() <= 1e-6 * np.abs(ref["fields"][i]).max(), name
+
+
+@pytest.mark.gpu
+def test_whole_run_with_eigen_constraint(oracle):
+    """Compliance (hard) + lowest-eigenvalue (soft, lower-sense) run on a
+    12x6x6 cantilever against the oracle's run: same stop reason, accepted-step
+    count within 2, and every accepted design meets the hard constraint."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2203_15115_b200.elements import Material
+
+    prob = opt.cantilever_problem(12, 6, 6, (12, 3, 3), (12, 3, 3),
+                                  constraints=[opt.ConstraintSpec("compliance", 1.6),
+                                               opt.ConstraintSpec("eigenvalue", 0.9, soft=True)])
+    prob.material = Material(E=1.0, nu=0.3, rho=1.0)
+    cfg = opt.OptimizerConfig(ersatz=1e-3, block=3, max_outer=10)
+    topo, hist, reason = opt.run(prob, cfg)
+    d, case, fixed, f = cantilever(12, 6, 6, (12, 3, 3), (12, 3, 3))
+    occ_r, hist_r, reason_r = oracle.run_optimizer(
+        12, 6, 6, [(fixed, f)], [{"kind": "compliance", "alpha": 1.6, "case": 0},
+                                 {"kind": "eigenvalue", "alpha": 0.9, "case": 0, "soft": True}],
+        block=3, ersatz=1e-3, max_outer=10)
+    assert reason == reason_r
+    acc = [h.v for h in hist if h.accepted]
+    acc_r = [h["v"] for h in hist_r if h["accepted"]]
+    assert abs(len(acc) - len(acc_r)) <= 2
+    names = list(hist[0].g)
+    assert all(h.g[names[0]] <= 1e-6 for h in hist if h.accepted)
