@@ -444,7 +444,8 @@ class NDCoarseSolver:
                 for r0 in range(0, nr, step):
                     bwd.append((ni, r0, min(nr, r0 + step)))
             bptr.append(len(bwd))
-        self.top_wpr = self._mode(self.n_top, np.array([self.n_top]))
+        self.top_wpr = (int(os.environ["TVB_ND_TOP_MODE"]) if os.environ.get("TVB_ND_TOP_MODE")
+                        else self._mode(self.n_top, np.array([self.n_top])))
         self.fwd_items = torch.from_numpy(np.array(fwd or [(0, 0, 0)], dtype=np.int32).reshape(-1, 3)).to(dev)
         self.bwd_items = torch.from_numpy(np.array(bwd or [(0, 0, 0)], dtype=np.int32).reshape(-1, 3)).to(dev)
         # device item records of the level schedule: the node's meta row, 0, row0, row1

@@ -146,6 +146,7 @@ static CoarseNDDev coarse_nd_dev(const tvb_coarse_nd* d) {
   D.cu_ld = d->cu_ld;
   D.ft_ld = d->ft_ld;
   D.max_cols = d->max_cols > 0 ? d->max_cols : 1;
+  D.top_smem = getenv("TVB_TOP_SMEM") ? atoi(getenv("TVB_TOP_SMEM")) : 0;
   return D;
 }
 

@@ -386,17 +386,27 @@ __device__ __forceinline__ void item_top_gather(const CoarseNDDev& D, int i0, in
 }
 
 // Top set, rows: x_T = S_T^-1 fT. ft: MC x n_top shared.
+// Per-level schedule: the top vector is read straight from global memory
+// (L1/L2-resident, written by the previous gather launch; kernel boundaries
+// make it coherent) -- staging it per CTA cost a serial fill + barrier in each
+// of the ~500 CTAs of this latency-bound launch. The persistent dataflow
+// kernel stages it through L2 (__ldcg): fT is written by other CTAs of the
+// same launch, so L1 could hold stale lines.
 template <int MC>
 __device__ __forceinline__ void item_top_rows(const CoarseNDDev& D, int wpr, int r0, int r1, const ColSet& C,
-                                              double* ft, double* red) {
+                                              double* ft, double* red, bool stage) {
   const int n = D.n_top;
-  fill_batched(ft, MC * n, [&](int i) {
-    const int c = i / n, k = i - c * n;
-    return __ldcg(D.fT + c * D.ft_ld + k);
-  });
-  __syncthreads();
   double d[MC];
-  rows_dot_w<MC>(wpr, D.ZT, n, ft, n, r0, r1, red, d);
+  if (stage) {
+    fill_batched(ft, MC * n, [&](int i) {
+      const int c = i / n, k = i - c * n;
+      return __ldcg(D.fT + c * D.ft_ld + k);
+    });
+    __syncthreads();
+    rows_dot_w<MC>(wpr, D.ZT, n, ft, n, r0, r1, red, d);
+  } else {
+    rows_dot_w<MC>(wpr, D.ZT, n, D.fT, (int)D.ft_ld, r0, r1, red, d);
+  }
   const int j = r0 + threadIdx.x;
   if (threadIdx.x < mode_rows(wpr) && j < r1)
 #pragma unroll
@@ -448,7 +458,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_flow(CoarseNDDev D, C
       case kAsm: item_asm<MC>(D, node_info(D.meta + 8 * node), C); break;
       case kRows: item_fwd<MC>(D, true, wpr, node_info(D.meta + 8 * node), r0, r1, C, sm, red); break;
       case kTopGather: item_top_gather<MC>(D, r0, r1, C); break;
-      case kTopRows: item_top_rows<MC>(D, wpr, r0, r1, C, sm, red); break;
+      case kTopRows: item_top_rows<MC>(D, wpr, r0, r1, C, sm, red, true); break;
       default: item_bwd<MC>(D, wpr, node_info(D.meta + 8 * node), r0, r1, C, sm, red); break;
     }
     __syncthreads();
@@ -515,7 +525,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_top_rows(CoarseNDDev 
   if (all_stopped<MC>(C)) return;
   const int rpc = mode_rows(D.top_wpr);
   const int r0 = blockIdx.x * rpc;
-  item_top_rows<MC>(D, D.top_wpr, r0, min(D.n_top, r0 + rpc), C, sm, red);
+  item_top_rows<MC>(D, D.top_wpr, r0, min(D.n_top, r0 + rpc), C, sm, red, D.top_smem != 0);
 }
 
 template <typename K>
@@ -583,7 +593,8 @@ static cudaError_t launch_coarse_cols(const CoarseNDDev& D, const ColSet& C, cud
   if (D.n_top > 0) {
     k_coarse_top_gather<MC><<<(unsigned)((D.n_top + 255) / 256), 256, 0, s>>>(D, C);
     const int rpc = kCoarseWarps * std::max(1, D.top_wpr >> 4) / (D.top_wpr & 15);
-    k_coarse_top_rows<MC><<<(unsigned)((D.n_top + rpc - 1) / rpc), kCoarseThreads, smem_top, s>>>(D, C);
+    k_coarse_top_rows<MC><<<(unsigned)((D.n_top + rpc - 1) / rpc), kCoarseThreads, D.top_smem ? smem_top : 0, s>>>(
+        D, C);
   }
   for (int h = 0; h < D.n_levels; ++h) {  // bwd groups: top-most bottom level first
     const long long a = D.bwd_ptr[h], b = D.bwd_ptr[h + 1];

@@ -43,6 +43,7 @@ struct CoarseNDDev {
   // multi-RHS scratch: column c of fS / cU / fT at + c * fs_ld / cu_ld / ft_ld
   long long fs_ld, cu_ld, ft_ld;
   int max_cols;               // scratch columns allocated (>= 1)
+  int top_smem;               // 1: stage the top vector in shared memory per CTA (TVB_TOP_SMEM=1, A/B only)
 };
 
 constexpr int kCoarseMaxCols = 4;  // right-hand sides per coarse-solve launch
