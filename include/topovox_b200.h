@@ -73,6 +73,14 @@ size_t tvb_matvec_host_ws_bytes(int nx, int ny, int nz);
 int tvb_matvec_host(int nx, int ny, int nz, const double* h_mh45, const double* h_u, double* h_out,
                     const double* d_occ, const uint8_t* d_nflags, int flags, int slabs, void* d_ws, size_t ws_bytes,
                     void* stream);
+/* A stream of nvec host vectors (h_u[v] -> h_out[v]) through the same slab
+ * pipeline, double-buffered on the device so vector v's host->device copies
+ * overlap vector v-1's device->host copies. Synchronous; results bitwise those
+ * of tvb_matvec_host. d_ws >= tvb_matvec_host_batch_ws_bytes() (4 vectors). */
+size_t tvb_matvec_host_batch_ws_bytes(int nx, int ny, int nz);
+int tvb_matvec_host_batch(int nx, int ny, int nz, const double* h_mh45, int nvec, const double* const* h_u,
+                          double* const* h_out, const double* d_occ, const uint8_t* d_nflags, int flags, int slabs,
+                          void* d_ws, size_t ws_bytes, void* stream);
 
 /* diagnostics: sustained fp64 FMA throughput of this GPU measured live
  * (independent DFMA chains on every SM), in TFLOP/s (2 flops per FMA);

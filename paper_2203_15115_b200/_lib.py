@@ -63,6 +63,8 @@ _SIGS = {
     "tvb_matvec_plan": (c_int, [c_int, c_int, c_int, P]),
     "tvb_matvec_host_ws_bytes": (c_size_t, [c_int, c_int, c_int]),
     "tvb_matvec_host": (c_int, [c_int, c_int, c_int, P, P, P, P, P, c_int, c_int, P, c_size_t, P]),
+    "tvb_matvec_host_batch_ws_bytes": (c_size_t, [c_int, c_int, c_int]),
+    "tvb_matvec_host_batch": (c_int, [c_int, c_int, c_int, P, c_int, P, P, P, P, c_int, c_int, P, c_size_t, P]),
     "tvb_fp64_peak_tflops": (c_double, [P]),
     "tvb_matvec_subset": (c_int, [c_int, c_int, c_int, P, P, P, P, c_ll, P, P, c_size_t, P]),
     "tvb_diag": (c_int, [c_int, c_int, c_int, P, P, P, P, c_int, P, P, P]),

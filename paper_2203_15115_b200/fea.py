@@ -164,6 +164,47 @@ class StiffnessOperator:
               "matvec (host buffers)")
         return out
 
+    def apply_host_batch(self, us, outs=None, raw: bool = False, slabs: int = 0):
+        """K @ u for a sequence of host vectors (numpy arrays or CPU float64
+        tensors, pinned for full overlap), streamed through the double-buffered
+        slab pipeline (``tvb_matvec_host_batch``): vector v+1's host->device
+        copies overlap vector v's device->host copies. Returns ``outs``
+        (allocated like the inputs when None); results are bitwise those of
+        ``apply_host``."""
+        torch = _torch()
+        us = list(us)
+        if outs is None:
+            outs = [torch.empty(self.n_dofs, dtype=torch.float64, pin_memory=u.is_pinned())
+                    if isinstance(u, torch.Tensor) else np.empty(self.n_dofs) for u in us]
+        outs = list(outs)
+        if len(outs) != len(us):
+            raise DimensionMismatch(f"{len(us)} input vectors but {len(outs)} outputs")
+        keep, pin, pout = [], [], []
+        for u, o in zip(us, outs):
+            for a, lst in ((u, pin), (o, pout)):
+                if isinstance(a, torch.Tensor):
+                    if a.dtype != torch.float64 or a.numel() != self.n_dofs or a.is_cuda or not a.is_contiguous():
+                        raise DimensionMismatch("host vectors must be contiguous CPU float64 of n_dofs entries")
+                    lst.append(a.data_ptr())
+                else:
+                    arr = a if lst is pout else np.ascontiguousarray(a, dtype=np.float64)
+                    if arr.shape != (self.n_dofs,) or arr.dtype != np.float64 or not arr.flags.c_contiguous:
+                        raise DimensionMismatch("host vectors must be contiguous float64 of n_dofs entries")
+                    keep.append(arr)
+                    lst.append(arr.ctypes.data)
+        need = lib().tvb_matvec_host_batch_ws_bytes(*self._dims())
+        if getattr(self, "_host_bws", None) is None or self._host_bws.numel() < need:
+            self._host_bws = torch.empty(need, dtype=torch.uint8, device="cuda")
+        flags = 0 if (raw or not self.dirichlet.size) else (_lib.MASK_IN | _lib.MASK_OUT)
+        n = len(us)
+        hu = (ctypes.c_void_p * max(n, 1))(*pin)
+        ho = (ctypes.c_void_p * max(n, 1))(*pout)
+        check(lib().tvb_matvec_host_batch(*self._dims(), self._mh.ctypes.data, n, ctypes.cast(hu, ctypes.c_void_p),
+                                          ctypes.cast(ho, ctypes.c_void_p), ptr(self.occ_d), ptr(self.nflags), flags,
+                                          int(slabs), ptr(self._host_bws), self._host_bws.numel(), stream_ptr()),
+              "matvec (host buffer batch)")
+        return outs
+
     def apply_subset(self, u, elems):
         """K @ u using only the listed elements (reference ``fea.py:67-76``)."""
         torch = _torch()
