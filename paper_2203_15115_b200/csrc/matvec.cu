@@ -96,6 +96,15 @@ __device__ __forceinline__ void xy_inverse(double (&f)[12]) {
     }
 }
 
+// TVB_MATVEC_DEBUG (compile-time): enables the TVB_MV_DEBUG stage switches
+// of the tuning experiments; compiled out otherwise (each was a per-step
+// uniform branch in the hot loop)
+#ifdef TVB_MATVEC_DEBUG
+#define TVB_MV_DBG(P) ((P).debug)
+#else
+#define TVB_MV_DBG(P) 0
+#endif
+
 constexpr int kStage = 4;   // max staged node-plane doubles per thread ((wy+1)*3(wx+1) <= kStage*NT)
 constexpr int kXcPad = 64;  // exchange rows past NT read (harmlessly) by edge threads
 constexpr int kAhead = 4;   // node planes in flight ahead of the compute (cp.async groups)
@@ -252,7 +261,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
     // sk = ring slot of plane / layer k; plane k+1 sits in sk+1, plane k+kAhead in sk-1 (mod kRing)
     auto step = [&](int k, int sk, const double (&bot)[12], double (&top)[12]) {
       const int sk1 = sk == kRing - 1 ? 0 : sk + 1, skl = sk == 0 ? kRing - 1 : sk - 1;
-      if (k + kAhead <= kz1 && !(P.debug & 2)) load_layer(k + kAhead, skl);
+      if (k + kAhead <= kz1 && !(TVB_MV_DBG(P) & 2)) load_layer(k + kAhead, skl);
       else cp_async_commit();  // keep one group per step
       gather_face(sk1, top);
       xy_forward(top);
@@ -290,7 +299,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
         for (int a = 0; a < 3; ++a) uo[a] = Up[sk * PS + j00 + S + 3 + a];
       }
       cp_async_wait_group<kAhead - 2>();  // plane k+2 (and occupancy k+2) landed
-      if (!(P.debug & 1)) __syncthreads();
+      if (!(TVB_MV_DBG(P) & 1)) __syncthreads();
       if (out) {
         // node (x0+tx, y0+ty) = local (1,1) of this column, (0,1) of column
         // tx+1, (1,0) of column ty+1 and (0,0) of column (tx+1, ty+1).
@@ -306,7 +315,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
           for (int a = 0; a < 3; ++a) {
             double w = ((fx >> a) & 1) ? 0.0 : v[a];
             if (P.accumulate) w += yrow[a];
-            if (!(P.debug & 4)) yrow[a] = w;
+            if (!(TVB_MV_DBG(P) & 4)) yrow[a] = w;
             if (DOT) dot = fma(uo[a], w, dot);
           }
         }
