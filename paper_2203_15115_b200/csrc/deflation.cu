@@ -305,9 +305,108 @@ __global__ void __launch_bounds__(kRestrictThreads) k_restrict(Agglo A, const ui
   }
 }
 
+// Warp-per-block variant: a 256-thread CTA restricts 8 blocks, one warp each
+// (lane-strided over the block's closed node box, 4 nodes' loads in flight per
+// lane, warp-shuffle trees, no shared memory or CTA barrier). Small blocks
+// (b = 4: 125 nodes) left the one-CTA-per-block kernel launch/latency-bound
+// (32768 CTAs of 128 threads at C2(b)).
+constexpr int kRestrictWarpThreads = 256;
+
+template <int BS>
+__global__ void __launch_bounds__(kRestrictWarpThreads) k_restrict_warp(Agglo A, const uint8_t* __restrict__ nflags,
+                                                                        DeflData D, const double* __restrict__ y,
+                                                                        const double* __restrict__ y2,
+                                                                        const SolverState* st, double* yc,
+                                                                        const int* stop) {
+  if (stop != nullptr && *stop) return;
+  const int lane = threadIdx.x & 31;
+  const long long B = (long long)blockIdx.x * (kRestrictWarpThreads / 32) + (threadIdx.x >> 5);
+  if (B >= A.nb) return;
+  const double beta = (y2 != nullptr) ? st->beta : 0.0;  // restrict y + beta*y2
+  const long long PB = D.perm != nullptr ? (long long)D.perm[B] : B;
+  const int keep = D.keep[B];
+  if (keep == 0) {
+    if (lane < 6) yc[6 * PB + lane] = 0.0;
+    return;
+  }
+  int bx, by, bz, nxl, nyl, nzl;
+  box_of(A, B, bx, by, bz, nxl, nyl, nzl);
+  const Grid& G = A.g;
+  const int X0 = A.b * bx, Y0 = A.b * by, Z0 = A.b * bz;
+  const double cx = D.cen[3 * B], cy = D.cen[3 * B + 1], cz = D.cen[3 * B + 2];
+  const int PX = BS > 0 ? BS + 1 : nxl, PY = BS > 0 ? BS + 1 : nyl, PZ = BS > 0 ? BS + 1 : nzl;
+  const int npos = PX * PY * PZ;
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  constexpr int kNodes = 4;
+  for (int i0 = lane; i0 < npos; i0 += kNodes * 32) {
+    uint8_t fl[kNodes];
+    double w[kNodes][3];
+    int lxs[kNodes], lys[kNodes], lzs[kNodes];
+#pragma unroll
+    for (int k = 0; k < kNodes; ++k) {
+      const int i = i0 + k * 32;
+      const int lx = i % PX, ly = (i / PX) % PY, lz = i / (PX * PY);
+      lxs[k] = lx;
+      lys[k] = ly;
+      lzs[k] = lz;
+      fl[k] = 0;
+      w[k][0] = w[k][1] = w[k][2] = 0.0;
+      if (i < npos && lx < nxl && ly < nyl && lz < nzl) {
+        const long long n = G.node(X0 + lx, Y0 + ly, Z0 + lz);
+        fl[k] = __ldg(nflags + n);
+        w[k][0] = __ldg(y + 3 * n);
+        w[k][1] = __ldg(y + 3 * n + 1);
+        w[k][2] = __ldg(y + 3 * n + 2);
+        if (y2 != nullptr) {
+          w[k][0] = fma(beta, __ldg(y2 + 3 * n), w[k][0]);
+          w[k][1] = fma(beta, __ldg(y2 + 3 * n + 1), w[k][1]);
+          w[k][2] = fma(beta, __ldg(y2 + 3 * n + 2), w[k][2]);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kNodes; ++k) {
+      if (!(fl[k] & kStructBit)) continue;
+      const double vx = (fl[k] & 1) ? 0.0 : w[k][0];
+      const double vy = (fl[k] & 2) ? 0.0 : w[k][1];
+      const double vz = (fl[k] & 4) ? 0.0 : w[k][2];
+      const double rx = A.h * (lxs[k] - cx), ry = A.h * (lys[k] - cy), rz = A.h * (lzs[k] - cz);
+      acc[0] += vx;
+      acc[1] += vy;
+      acc[2] += vz;
+      acc[3] += ry * vz - rz * vy;
+      acc[4] += rz * vx - rx * vz;
+      acc[5] += rx * vy - ry * vx;
+    }
+  }
+  double m[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) m[k] = __shfl_sync(0xffffffffu, warp_sum(acc[k]), 0);
+  if (lane < 6) {
+    const double* S = D.S + 36 * B;
+    double v = 0.0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) v = fma(S[i + 6 * lane], m[i], v);
+    yc[6 * PB + lane] = v;
+  }
+}
+
 cudaError_t launch_restrict(const Agglo& A, const uint8_t* nflags, DeflData D, const double* y, double* yc,
                             cudaStream_t s, const int* stop, const double* y2, const void* state) {
   const SolverState* st = (const SolverState*)state;
+  static int mode = -1;  // TVB_RESTRICT=cta|warp (A/B); default: warp per block below 8^3 blocks
+  if (mode < 0) {
+    const char* e = getenv("TVB_RESTRICT");
+    mode = e == nullptr ? 0 : (e[0] == 'w' ? 1 : 2);
+  }
+  const bool warp = mode == 1 || (mode == 0 && A.b < 8);
+  if (warp) {
+    const unsigned gw = (unsigned)((A.nb + 7) / 8);
+    if (A.b == 8) k_restrict_warp<8><<<gw, kRestrictWarpThreads, 0, s>>>(A, nflags, D, y, y2, st, yc, stop);
+    else if (A.b == 4) k_restrict_warp<4><<<gw, kRestrictWarpThreads, 0, s>>>(A, nflags, D, y, y2, st, yc, stop);
+    else k_restrict_warp<0><<<gw, kRestrictWarpThreads, 0, s>>>(A, nflags, D, y, y2, st, yc, stop);
+    return cudaGetLastError();
+  }
   const unsigned g = (unsigned)A.nb;
   if (A.b == 8) k_restrict<8><<<g, kRestrictThreads, 0, s>>>(A, nflags, D, y, y2, st, yc, stop);
   else if (A.b == 4) k_restrict<4><<<g, kRestrictThreads, 0, s>>>(A, nflags, D, y, y2, st, yc, stop);
