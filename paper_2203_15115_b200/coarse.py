@@ -50,8 +50,10 @@ log = logging.getLogger(__name__)
 #: fronts larger than this (DOFs) get a separate assembly pass in the forward solve
 SPLIT_FRONT = int(os.environ.get("TVB_ND_SPLIT_FRONT", "2048"))
 #: largest top set inverted densely (DOFs); the top tree levels it replaces
-#: would otherwise cost two latency-bound launches each
-TOP_MAX = int(os.environ.get("TVB_ND_TOP_MAX", "4608"))
+#: would otherwise cost two latency-bound launches each. 6200 admits the
+#: 6144-DOF top separator of C2(b) (2247 -> 2200 us per iteration); C4 (3738)
+#: and C5 (2400) are unchanged; 13000 was slower at C2(b), 2500 at C4 (+5 %)
+TOP_MAX = int(os.environ.get("TVB_ND_TOP_MAX", "6200"))
 #: largest leaf box of the dissection (blocks); default by size: 125 for
 #: coarse systems up to FLOW_MIN_DOFS (fewer, fatter tree levels: C4 coarse
 #: solve 86 -> 66 us in the iteration), 64 above (C5 / C2(b) are bandwidth-bound)
