@@ -183,6 +183,13 @@ typedef struct tvb_coarse_nd {
      max_cols columns allocated (solves of more RHS run in groups of max_cols) */
   long long fs_ld, cu_ld, ft_ld;
   int max_cols;
+  /* packed symmetric top (per-level schedule only): top_tiles = ceil(n_top/64)
+     > 0 -> d_ZT holds the lower 64x64 tiles (I >= J at I*(I+1)/2 + J,
+     row-major, zero-padded) and d_tpart (max_cols x [nt][nt][64], column
+     stride tpart_ld) receives the tile partial products; 0 -> dense rows */
+  int top_tiles;
+  double* d_tpart;
+  long long tpart_ld;
 } tvb_coarse_nd;
 int tvb_coarse_nd_solve(const tvb_coarse_nd* nd, const double* d_y, double* d_x, void* stream);
 

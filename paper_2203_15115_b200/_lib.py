@@ -37,6 +37,7 @@ class CoarseND(ctypes.Structure):
         ("d_factor", P), ("factor_bytes", c_size_t),
         ("fs_ld", ctypes.c_longlong), ("cu_ld", ctypes.c_longlong), ("ft_ld", ctypes.c_longlong),
         ("max_cols", c_int),
+        ("top_tiles", c_int), ("d_tpart", P), ("tpart_ld", ctypes.c_longlong),
     ]
 
 

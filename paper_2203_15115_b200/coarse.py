@@ -72,6 +72,10 @@ SMEM_MAX = 227 * 1024
 #: right-hand sides per coarse-solve launch (coarse.cu kCoarseMaxCols); the
 #: scratch vectors fS / cU / fT carry this many columns
 MAX_COLS = 4
+#: symmetric top inverse stored as its lower 64x64 tiles (half the bytes read
+#: per solve; coarse.cu k_top_tiles / k_top_reduce); TVB_ND_PACK_TOP=0 -> dense rows
+TOP_TILE = 64
+PACK_TOP = os.environ.get("TVB_ND_PACK_TOP", "1") != "0"
 #: resident 256-thread CTAs on the GPU (148 SMs x 8): one wave of solve items
 CTA_SLOTS = int(os.environ.get("TVB_ND_SLOTS", "1184"))
 #: index plans of the numeric factorisation, keyed by (block grid, leaf, top, device)
@@ -194,6 +198,9 @@ class NDCoarseSolver:
                 self._bkids[bidx[p]].append(k)
             elif p >= 0:
                 self._top_parent[k] = True
+        self.flow = FLOW != "0" if FLOW is not None else 6 * nb >= FLOW_MIN_DOFS
+        #: packed symmetric top tiles (per-level schedule; the dataflow kernel reads dense rows)
+        self.top_tiles = (self.n_top + TOP_TILE - 1) // TOP_TILE if (self.n_top and not self.flow and PACK_TOP) else 0
         self._factor(torch, Es, nodes, bottom, top, bidx, perm)
         self._make = make_desc
         self.desc = self._make_desc() if make_desc else None
@@ -378,7 +385,8 @@ class NDCoarseSolver:
             g_off[1:] = np.cumsum(s * u)
             b_off[1:] = np.cumsum(s * (s + u))
         ng, nbb = int(g_off[-1]), int(b_off[-1])
-        ntop2 = self.n_top * self.n_top
+        nt = self.top_tiles
+        ntop2 = nt * (nt + 1) // 2 * TOP_TILE * TOP_TILE if nt else self.n_top * self.n_top
         # G, [Z | -G^T] and the dense top inverse in ONE allocation
         self.factor = torch.zeros(ng + nbb + ntop2 + 3, dtype=torch.float64, device=dev)
         self.G = self.factor[:ng + 1]
@@ -388,8 +396,20 @@ class NDCoarseSolver:
             self.G[:ng] = torch.cat([g.reshape(-1) for g in G_list])
         if nbb:
             self.B[:nbb] = torch.cat([b.reshape(-1) for b in B_list])
-        if ntop2:
+        if ntop2 and nt:
+            # lower 64x64 tiles of the (symmetric) inverse, tile I*(I+1)/2 + J, row-major, zero-padded
+            n = self.n_top
+            Zp = torch.zeros(nt * TOP_TILE, nt * TOP_TILE, dtype=torch.float64, device=dev)
+            Zp[:n, :n] = self.Ztop
+            tiles = Zp.view(nt, TOP_TILE, nt, TOP_TILE).permute(0, 2, 1, 3)
+            Ii, Jj = np.tril_indices(nt)
+            self.ZT[:ntop2] = tiles[torch.from_numpy(Ii).to(dev), torch.from_numpy(Jj).to(dev)].reshape(-1)
+            del Zp, tiles
+            self.tpart = torch.zeros(MAX_COLS, nt * nt * TOP_TILE, dtype=torch.float64, device=dev)
+        elif ntop2:
             self.ZT[:ntop2] = self.Ztop.reshape(-1)
+        if not nt:
+            self.tpart = None
         self.Ztop = None
         ud_off = np.zeros(nbot + 1, dtype=np.int64)
         if nbot:
@@ -583,13 +603,14 @@ class NDCoarseSolver:
         d.d_ZT, d.d_fT = ptr(self.ZT), ptr(self.fT)
         d.d_tptr, d.d_tidx = ptr(self.tptr), ptr(self.tidx)
         d.d_perm = ptr(self.perm)
-        flow = FLOW != "0" if FLOW is not None else 6 * self.nb >= FLOW_MIN_DOFS
-        if flow:
+        if self.flow:
             d.d_items, d.n_items, d.d_rel = ptr(self.items), self.n_items, ptr(self.rel)
             d.d_cnt, d.d_ctl = ptr(self.cnt), ptr(self.ctl)
         d.d_factor, d.factor_bytes = ptr(self.factor), self.bytes
         d.fs_ld, d.cu_ld, d.ft_ld = self.fS.shape[1], self.cU.shape[1], self.fT.shape[1]
         d.max_cols = self.max_cols
+        if self.top_tiles:
+            d.top_tiles, d.d_tpart, d.tpart_ld = self.top_tiles, ptr(self.tpart), self.tpart.shape[1]
         return d
 
     def solve_device(self, y, x):

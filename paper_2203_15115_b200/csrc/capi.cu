@@ -147,6 +147,9 @@ static CoarseNDDev coarse_nd_dev(const tvb_coarse_nd* d) {
   D.ft_ld = d->ft_ld;
   D.max_cols = d->max_cols > 0 ? d->max_cols : 1;
   D.top_smem = getenv("TVB_TOP_SMEM") ? atoi(getenv("TVB_TOP_SMEM")) : 0;
+  D.top_tiles = (d->d_items == nullptr || d->n_items <= 0) ? d->top_tiles : 0;
+  D.tpart = d->d_tpart;
+  D.tpart_ld = d->tpart_ld;
   return D;
 }
 

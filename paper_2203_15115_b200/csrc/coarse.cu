@@ -413,6 +413,106 @@ __device__ __forceinline__ void item_top_rows(const CoarseNDDev& D, int wpr, int
     for (int c = 0; c < MC; ++c) C.x[c * C.ldx + D.top_off + j] = d[c];
 }
 
+// ---- packed symmetric top: x_T = S_T^-1 f_T from the lower tiles -----------
+// Tile (I, J), J <= I, is read once and serves both products it appears in:
+// rows  P[I][J] = T_IJ f_J            (64 partials of block row I)
+// cols  P[J][I] = T_IJ^T f_I  (J < I) (64 partials of block row J)
+// and k_top_reduce sums x_I = sum_J P[I][J] in J order. Half the bytes of the
+// dense inverse; fixed summation order (deterministic).
+constexpr int kTopTile = 64;
+
+__device__ __forceinline__ void tile_ij(long long t, int& I, int& J) {
+  int i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((long long)(i + 1) * (i + 2) / 2 <= t) ++i;
+  while ((long long)i * (i + 1) / 2 > t) --i;
+  I = i;
+  J = (int)(t - (long long)i * (i + 1) / 2);
+}
+
+template <int MC>
+__global__ void __launch_bounds__(kCoarseThreads) k_top_tiles(CoarseNDDev D, ColSet C) {
+  __shared__ double colp[kCoarseWarps][MC][kTopTile];
+  if (all_stopped<MC>(C)) return;
+  int I, J;
+  tile_ij(blockIdx.x, I, J);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = D.n_top, nt = D.top_tiles;
+  const double* T = D.ZT + (long long)blockIdx.x * kTopTile * kTopTile;
+  constexpr int RW = kTopTile / kCoarseWarps;  // rows per warp (8)
+  // the warp's 8 rows x 64 columns: 16 independent loads per lane
+  double a[RW][2];
+#pragma unroll
+  for (int q = 0; q < RW; ++q) {
+    a[q][0] = __ldg(T + (warp * RW + q) * kTopTile + lane);
+    a[q][1] = __ldg(T + (warp * RW + q) * kTopTile + lane + 32);
+  }
+  double fj[MC][2], fi[MC][RW];
+#pragma unroll
+  for (int c = 0; c < MC; ++c) {
+    const double* f = D.fT + c * D.ft_ld;
+    const int j0 = J * kTopTile + lane, j1 = j0 + 32;
+    fj[c][0] = j0 < n ? __ldcg(f + j0) : 0.0;
+    fj[c][1] = j1 < n ? __ldcg(f + j1) : 0.0;
+#pragma unroll
+    for (int q = 0; q < RW; ++q) {
+      const int i = I * kTopTile + warp * RW + q;
+      fi[c][q] = (I != J && i < n) ? __ldcg(f + i) : 0.0;
+    }
+  }
+  double* P = D.tpart;
+#pragma unroll
+  for (int c = 0; c < MC; ++c) {
+    double* Pc = P + c * D.tpart_ld;
+#pragma unroll
+    for (int q = 0; q < RW; ++q) {
+      const double r = warp_sum(fma(a[q][1], fj[c][1], a[q][0] * fj[c][0]));
+      if (lane == 0) Pc[((long long)I * nt + J) * kTopTile + warp * RW + q] = r;
+    }
+    if (I != J) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < RW; ++q) {
+        s0 = fma(a[q][0], fi[c][q], s0);
+        s1 = fma(a[q][1], fi[c][q], s1);
+      }
+      colp[warp][c][lane] = s0;
+      colp[warp][c][lane + 32] = s1;
+    }
+  }
+  if (I == J) return;
+  __syncthreads();
+  if (threadIdx.x < kTopTile) {
+#pragma unroll
+    for (int c = 0; c < MC; ++c) {
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < kCoarseWarps; ++w) v += colp[w][c][threadIdx.x];
+      P[c * D.tpart_ld + ((long long)J * nt + I) * kTopTile + threadIdx.x] = v;
+    }
+  }
+}
+
+// x_I[r] = sum_J P[I][J][r]: 4 threads per row, each a contiguous J quarter
+// (its loads all in flight), combined in a fixed shuffle order.
+template <int MC>
+__global__ void __launch_bounds__(kCoarseThreads) k_top_reduce(CoarseNDDev D, ColSet C) {
+  if (all_stopped<MC>(C)) return;
+  const int nt = D.top_tiles;
+  const int I = blockIdx.x;
+  const int r = threadIdx.x >> 2, part = threadIdx.x & 3;
+  const int per = (nt + 3) / 4, j0 = part * per, j1 = min(nt, j0 + per);
+#pragma unroll
+  for (int c = 0; c < MC; ++c) {
+    const double* Pc = D.tpart + c * D.tpart_ld + (long long)I * nt * kTopTile + r;
+    double s = 0.0;
+    for (int j = j0; j < j1; ++j) s += __ldcg(Pc + (long long)j * kTopTile);
+    s += __shfl_down_sync(0xffffffffu, s, 1);
+    s += __shfl_down_sync(0xffffffffu, s, 2);
+    const int i = I * kTopTile + r;
+    if (part == 0 && i < D.n_top) C.x[c * C.ldx + D.top_off + i] = s;
+  }
+}
+
 // ---- persistent dataflow schedule -------------------------------------------
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
   unsigned long long v;
@@ -590,7 +690,12 @@ static cudaError_t launch_coarse_cols(const CoarseNDDev& D, const ColSet& C, cud
     k_coarse_fwd<MC><<<(unsigned)(b - a), kCoarseThreads, smem_fwd, s>>>(D, D.fwd_wpr[h], split,
                                                                          D.fwd_items + 10 * a, C);
   }
-  if (D.n_top > 0) {
+  if (D.n_top > 0 && D.top_tiles > 0) {
+    k_coarse_top_gather<MC><<<(unsigned)((D.n_top + 255) / 256), 256, 0, s>>>(D, C);
+    const long long ntiles = (long long)D.top_tiles * (D.top_tiles + 1) / 2;
+    k_top_tiles<MC><<<(unsigned)ntiles, kCoarseThreads, 0, s>>>(D, C);
+    k_top_reduce<MC><<<(unsigned)D.top_tiles, kCoarseThreads, 0, s>>>(D, C);
+  } else if (D.n_top > 0) {
     k_coarse_top_gather<MC><<<(unsigned)((D.n_top + 255) / 256), 256, 0, s>>>(D, C);
     const int rpc = kCoarseWarps * std::max(1, D.top_wpr >> 4) / (D.top_wpr & 15);
     k_coarse_top_rows<MC><<<(unsigned)((D.n_top + rpc - 1) / rpc), kCoarseThreads, D.top_smem ? smem_top : 0, s>>>(

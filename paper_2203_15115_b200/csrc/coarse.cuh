@@ -44,6 +44,12 @@ struct CoarseNDDev {
   long long fs_ld, cu_ld, ft_ld;
   int max_cols;               // scratch columns allocated (>= 1)
   int top_smem;               // 1: stage the top vector in shared memory per CTA (TVB_TOP_SMEM=1, A/B only)
+  // packed symmetric top (per-level schedule): ZT holds the lower 64x64 tiles
+  // (I >= J, tile I*(I+1)/2 + J, row-major, zero-padded) instead of the dense
+  // n_top^2 inverse; tpart: per-column [nt][nt][64] tile partial products
+  int top_tiles;              // nt = ceil(n_top / 64); 0 = dense rows
+  double* tpart;
+  long long tpart_ld;
 };
 
 constexpr int kCoarseMaxCols = 4;  // right-hand sides per coarse-solve launch

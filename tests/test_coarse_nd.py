@@ -76,7 +76,19 @@ def emulate_solve(nd, y):
         n = nd.n_top
         tptr, tidx = nd.tptr.numpy(), nd.tidx.numpy()
         fT = np.array([y[nd.top_off + i] + cU[tidx[tptr[i]:tptr[i + 1]]].sum() for i in range(n)])
-        x[nd.top_off:] = ZT[:n * n].reshape(n, n) @ fT
+        if nd.top_tiles:  # k_top_tiles + k_top_reduce over the packed lower tiles
+            nt, ts = nd.top_tiles, 64
+            fp = np.zeros(nt * ts)
+            fp[:n] = fT
+            tiles = ZT[:nt * (nt + 1) // 2 * ts * ts].reshape(-1, ts, ts)
+            P = np.zeros((nt, nt, ts))
+            for t, (I, J) in enumerate(zip(*np.tril_indices(nt))):
+                P[I, J] = tiles[t] @ fp[J * ts:(J + 1) * ts]
+                if I != J:
+                    P[J, I] = tiles[t].T @ fp[I * ts:(I + 1) * ts]
+            x[nd.top_off:] = P.sum(axis=1).reshape(-1)[:n]
+        else:
+            x[nd.top_off:] = ZT[:n * n].reshape(n, n) @ fT
     for node, r0, r1 in bwd:  # k_coarse_bwd, top-most bottom level first
         s, u, g, b, so, uo, gm, _ = meta[node]
         Bm = B[b:b + s * (s + u)].reshape(s, s + u)
@@ -186,6 +198,7 @@ def test_nd_dataflow_schedule(grid, leaf, top_max, monkeypatch):
     import paper_2203_15115_b200.coarse as C
 
     monkeypatch.setattr(C, "SPLIT_FRONT", 200)  # exercise the assembly items too
+    monkeypatch.setattr(C, "FLOW", "1")  # the dataflow kernel reads the dense top rows (no packed tiles)
     mx, my, mz = grid
     Es = random_block_stencil(mx, my, mz, seed=sum(grid) + 1)
     E = dense_of(Es, mx, my, mz)
