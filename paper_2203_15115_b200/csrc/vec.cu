@@ -6,6 +6,9 @@
 // contiguous slice with a warp-shuffle tree, writes its partial, and the last
 // CTA to finish (device counter) sums the partials in index order. Results are
 // therefore bitwise reproducible for a given launch geometry.
+#include <algorithm>
+#include <cstdlib>
+
 #include "vec.cuh"
 
 namespace tvb {
@@ -345,10 +348,24 @@ cudaError_t launch_pcg_update(long long n, double* x, double* r, double* z, cons
   const bool vec16 = (((x ? reinterpret_cast<uintptr_t>(x) : 0) | reinterpret_cast<uintptr_t>(r) |
                        reinterpret_cast<uintptr_t>(z) | reinterpret_cast<uintptr_t>(p) |
                        reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(inv_d)) & 15) == 0;
+  // grid: at most 4 CTAs per SM, an exact multiple of the SM count for large
+  // vectors (C4: 774 -> 592 CTAs, 218.3 -> 213 us per DPCG iteration; 8 and
+  // 2 per SM were slower); TVB_UPD_CTAS overrides (A/B experiments)
+  static int upd_ctas = -1;
+  if (upd_ctas < 0) {
+    upd_ctas = getenv("TVB_UPD_CTAS") ? atoi(getenv("TVB_UPD_CTAS")) : 0;
+    if (upd_ctas <= 0) {
+      int dev = 0, nsm = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      upd_ctas = 4 * nsm;
+    }
+  }
+  const int g = std::min(std::min(upd_ctas, kMaxReduceCtas), reduce_grid(n));
   if (vec16 && x != nullptr) {
-    k_pcg_update_v2<true><<<reduce_grid(n), 256, 0, s>>>(n, x, r, z, p, q, inv_d, st, partials, pq_parts, n_parts);
+    k_pcg_update_v2<true><<<g, 256, 0, s>>>(n, x, r, z, p, q, inv_d, st, partials, pq_parts, n_parts);
   } else if (vec16) {
-    k_pcg_update_v2<false><<<reduce_grid(n), 256, 0, s>>>(n, x, r, z, p, q, inv_d, st, partials, pq_parts, n_parts);
+    k_pcg_update_v2<false><<<g, 256, 0, s>>>(n, x, r, z, p, q, inv_d, st, partials, pq_parts, n_parts);
   } else {
     if (pq_parts != nullptr) k_finalize_pq<<<1, 256, 0, s>>>(pq_parts, n_parts, st);
     k_pcg_update<<<reduce_grid(n), 256, 0, s>>>(n, x, r, z, p, q, inv_d, st, partials);
