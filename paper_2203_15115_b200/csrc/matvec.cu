@@ -359,8 +359,12 @@ static size_t matvec_smem(int nt, int wx, int wy) {
 static int ctas_per_sm(int nt) { return nt == 256 ? 2 : 1; }
 
 // Tile choice for the persistent balanced split: per-SM time ~ (tile work of
-// all pz planes + one halo layer per piece) x warps / resident CTAs. Redundant
-// halo columns and empty tile parts count as work.
+// all pz planes + one halo layer per piece) x the CTA's warps (all NT/32 warps
+// stage, exchange and synchronise, even where a tile leaves threads idle) /
+// CTAs. Redundant halo columns and empty tile parts count as work; ties go to
+// the longer staged rows (larger wx). Measured against the previous
+// active-warp count (which tied 22x10 with 24x10 at C4): C4 39.9 -> 36.9 us,
+// C5 197.6 -> 187-193 us, C2 unchanged (23x11).
 // TVB_MV_PLAN="nt,wx,wy[,ctas]" overrides (tuning sweeps).
 MatvecPlan plan_matvec(const Grid& g, int num_sms) {
   if (const char* e = getenv("TVB_MV_PLAN")) {
@@ -375,7 +379,7 @@ MatvecPlan plan_matvec(const Grid& g, int num_sms) {
   MatvecPlan best{};
   double best_cost = 1e300;
   // wx < 20 loses to short staged rows and frequent warp row-wraps (measured
-  // sweeps, profiles/README.md); nt = 512 never won.
+  // sweeps, profiles/README.md); nt = 384 / 512 never won.
   for (int nt : {256, 384}) {
     const int nc = num_sms * ctas_per_sm(nt);
     for (int wx = 20; wx <= 48; ++wx) {
@@ -384,10 +388,10 @@ MatvecPlan plan_matvec(const Grid& g, int num_sms) {
         const int ntx = (g.px + wx - 2) / (wx - 1);
         const int nty = (g.py + wy - 2) / (wy - 1);
         const double tiles = (double)ntx * nty;
-        const int warps = (wx * wy + 31) / 32;
+        const int warps = nt / 32;
         const double pieces = std::max(tiles, (double)nc) + nc;  // upper bound of pieces
-        const double cost = (tiles * g.pz + 1.5 * pieces) * warps / nc / ctas_per_sm(nt);
-        if (cost < best_cost - 1e-9) {
+        const double cost = (tiles * g.pz + 1.5 * pieces) * warps / nc;
+        if (cost < best_cost - 1e-9 || (cost <= best_cost + 1e-9 && wx > best.wx)) {
           best_cost = cost;
           best = MatvecPlan{nt, wx, wy, ntx, nty, nc, matvec_smem(nt, wx, wy)};
         }
