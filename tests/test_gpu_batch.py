@@ -150,3 +150,35 @@ def test_batch_c4_two_load_cases(tv):
         single = fea.solve_static(op, F[c], tol=1e-8, deflation=defl)
         assert batch[c].iterations == single.iterations
         assert torch.equal(batch[c].u, single.u)
+
+
+@pytest.mark.parametrize("flow", ["1", "0"])
+def test_batch_nd_tree_schedules(tv, flow, monkeypatch):
+    """Multi-column coarse solve through a real bottom tree (small dense top),
+    with the persistent dataflow kernel (flow = 1, used from 48k coarse DOFs
+    at full size) and with the per-level launches + packed top tiles: every
+    column bitwise equals its single solve, and the ND solution matches the
+    dense coarse inverse's."""
+    import torch
+
+    import paper_2203_15115_b200.coarse as C
+    from paper_2203_15115_b200 import fea
+
+    monkeypatch.setattr(C, "FLOW", flow)
+    monkeypatch.setattr(C, "TOP_MAX", 200)
+    monkeypatch.setattr(C, "LEAF_MAX", 8)
+    d, fixed, f, occ, op = _problem(tv, (32, 16, 16), 0.9, 9)
+    defl = fea.build_deflation(d, op.topology, fixed, 4, coarse="nd")
+    defl.prepare(op)
+    assert defl.nd.H0 >= 1 and defl.nd.n_top > 0
+    assert (defl.nd.top_tiles > 0) == (flow == "0")
+    F = [torch.from_numpy(v).cuda() for v in _forces(d, fixed, f, 3, 5)]
+    batch = fea.solve_static_batch(op, F, tol=1e-12, deflation=defl)
+    for c in range(3):
+        single = fea.solve_static(op, F[c], tol=1e-12, deflation=defl)
+        assert batch[c].iterations == single.iterations
+        assert torch.equal(batch[c].u, single.u)
+    dense = fea.build_deflation(d, op.topology, fixed, 4, coarse="dense")
+    rd = fea.solve_static(op, F[0], tol=1e-12, deflation=dense)
+    assert abs(rd.iterations - batch[0].iterations) <= 1
+    assert rel(batch[0].u.cpu().numpy(), rd.u.cpu().numpy()) < 1e-10
