@@ -431,6 +431,7 @@ __device__ __forceinline__ void tile_ij(long long t, int& I, int& J) {
 
 template <int MC>
 __global__ void __launch_bounds__(kCoarseThreads) k_top_tiles(CoarseNDDev D, ColSet C) {
+  pdl_entry();
   __shared__ double colp[kCoarseWarps][MC][kTopTile];
   if (all_stopped<MC>(C)) return;
   int I, J;
@@ -496,6 +497,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_top_tiles(CoarseNDDev D, Col
 // (its loads all in flight), combined in a fixed shuffle order.
 template <int MC>
 __global__ void __launch_bounds__(kCoarseThreads) k_top_reduce(CoarseNDDev D, ColSet C) {
+  pdl_entry();
   if (all_stopped<MC>(C)) return;
   const int nt = D.top_tiles;
   const int I = blockIdx.x;
@@ -524,6 +526,7 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 // done_idx, done_need, rel_begin, rel_end, 0
 template <int MC>
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_flow(CoarseNDDev D, ColSet C) {
+  pdl_entry();
   extern __shared__ double sm[];
   __shared__ double red[MC * kRedStride];
   __shared__ int s_item;
@@ -587,6 +590,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_flow(CoarseNDDev D, C
 template <int MC>
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_fwd(CoarseNDDev D, int wpr, int assembled,
                                                                const long long* recs, ColSet C) {
+  pdl_entry();
   extern __shared__ double sm[];
   __shared__ double red[MC * kRedStride];
   if (all_stopped<MC>(C)) return;
@@ -597,6 +601,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_fwd(CoarseNDDev D, in
 
 template <int MC>
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_asm(CoarseNDDev D, const int* nodes, ColSet C) {
+  pdl_entry();
   if (all_stopped<MC>(C)) return;
   item_asm<MC>(D, node_info(D.meta + 8 * nodes[blockIdx.x]), C);
 }
@@ -604,6 +609,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_asm(CoarseNDDev D, co
 template <int MC>
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_bwd(CoarseNDDev D, int wpr, const long long* recs,
                                                                ColSet C) {
+  pdl_entry();
   extern __shared__ double sm[];
   __shared__ double red[MC * kRedStride];
   if (all_stopped<MC>(C)) return;
@@ -614,12 +620,14 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_bwd(CoarseNDDev D, in
 
 template <int MC>
 __global__ void k_coarse_top_gather(CoarseNDDev D, ColSet C) {
+  pdl_entry();
   if (all_stopped<MC>(C)) return;
   item_top_gather<MC>(D, blockIdx.x * blockDim.x, D.n_top, C);
 }
 
 template <int MC>
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_top_rows(CoarseNDDev D, ColSet C) {
+  pdl_entry();
   extern __shared__ double sm[];
   __shared__ double red[MC * kRedStride];
   if (all_stopped<MC>(C)) return;
@@ -676,7 +684,7 @@ static cudaError_t launch_coarse_cols(const CoarseNDDev& D, const ColSet& C, cud
       cached_smem = smem_max;
     }
     const int ctas = std::min(cached_ctas, D.n_items);
-    k_coarse_flow<MC><<<(unsigned)ctas, kCoarseThreads, smem_max, s>>>(D, C);
+    launch_k(k_coarse_flow<MC>, (unsigned)ctas, kCoarseThreads, smem_max, s, D, C);
     return cudaGetLastError();
   }
   for (int h = 0; h < D.n_levels; ++h) {
@@ -685,26 +693,26 @@ static cudaError_t launch_coarse_cols(const CoarseNDDev& D, const ColSet& C, cud
     const int split = D.split[h] != 0;
     if (split) {
       const long long na = D.asm_ptr[h], nb = D.asm_ptr[h + 1];
-      k_coarse_asm<MC><<<(unsigned)(nb - na), kCoarseThreads, 0, s>>>(D, D.asm_nodes + na, C);
+      launch_k(k_coarse_asm<MC>, (unsigned)(nb - na), kCoarseThreads, 0, s, D, D.asm_nodes + na, C);
     }
-    k_coarse_fwd<MC><<<(unsigned)(b - a), kCoarseThreads, smem_fwd, s>>>(D, D.fwd_wpr[h], split,
+    launch_k(k_coarse_fwd<MC>, (unsigned)(b - a), kCoarseThreads, smem_fwd, s, D, D.fwd_wpr[h], split,
                                                                          D.fwd_items + 10 * a, C);
   }
   if (D.n_top > 0 && D.top_tiles > 0) {
-    k_coarse_top_gather<MC><<<(unsigned)((D.n_top + 255) / 256), 256, 0, s>>>(D, C);
+    launch_k(k_coarse_top_gather<MC>, (unsigned)((D.n_top + 255) / 256), 256, 0, s, D, C);
     const long long ntiles = (long long)D.top_tiles * (D.top_tiles + 1) / 2;
-    k_top_tiles<MC><<<(unsigned)ntiles, kCoarseThreads, 0, s>>>(D, C);
-    k_top_reduce<MC><<<(unsigned)D.top_tiles, kCoarseThreads, 0, s>>>(D, C);
+    launch_k(k_top_tiles<MC>, (unsigned)ntiles, kCoarseThreads, 0, s, D, C);
+    launch_k(k_top_reduce<MC>, (unsigned)D.top_tiles, kCoarseThreads, 0, s, D, C);
   } else if (D.n_top > 0) {
-    k_coarse_top_gather<MC><<<(unsigned)((D.n_top + 255) / 256), 256, 0, s>>>(D, C);
+    launch_k(k_coarse_top_gather<MC>, (unsigned)((D.n_top + 255) / 256), 256, 0, s, D, C);
     const int rpc = kCoarseWarps * std::max(1, D.top_wpr >> 4) / (D.top_wpr & 15);
-    k_coarse_top_rows<MC><<<(unsigned)((D.n_top + rpc - 1) / rpc), kCoarseThreads, D.top_smem ? smem_top : 0, s>>>(
+    launch_k(k_coarse_top_rows<MC>, (unsigned)((D.n_top + rpc - 1) / rpc), kCoarseThreads, D.top_smem ? smem_top : 0, s,
         D, C);
   }
   for (int h = 0; h < D.n_levels; ++h) {  // bwd groups: top-most bottom level first
     const long long a = D.bwd_ptr[h], b = D.bwd_ptr[h + 1];
     if (b > a)
-      k_coarse_bwd<MC><<<(unsigned)(b - a), kCoarseThreads, smem_bwd, s>>>(D, D.bwd_wpr[h], D.bwd_items + 10 * a, C);
+      launch_k(k_coarse_bwd<MC>, (unsigned)(b - a), kCoarseThreads, smem_bwd, s, D, D.bwd_wpr[h], D.bwd_items + 10 * a, C);
   }
   return cudaGetLastError();
 }

@@ -8,7 +8,9 @@
 // No index table is ever read: every index is arithmetic in (nx, ny, nz).
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
+#include <utility>
 
 namespace tvb {
 
@@ -109,6 +111,47 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <int N>
 __device__ __forceinline__ void cp_async_wait_group() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Programmatic dependent launch (sm_90+) ------------------------------------
+// Every kernel of the solver iteration starts with pdl_entry(): it lets the
+// next kernel in the stream launch as soon as all of this grid's CTAs are
+// resident (launch_dependents), then blocks until the previous grid has
+// completed and its writes are visible (wait). So the next kernel's launch
+// and CTA rasterisation overlap this kernel's run instead of following its
+// completion, and no kernel touches its predecessor's data early. Both
+// instructions are no-ops for a grid launched without the PDL attribute.
+// All CTAs of a grid are resident before its dependents can launch, so
+// early-launched CTAs can never starve their predecessor of SM slots.
+__device__ __forceinline__ void pdl_entry() {
+#ifdef TVB_PDL_EARLY
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#endif
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
+// TVB_PDL=0 launches without the attribute (A/B experiments).
+inline bool pdl_enabled() {
+  static const int on = getenv("TVB_PDL") ? atoi(getenv("TVB_PDL")) : 1;
+  return on != 0;
+}
+
+// kernel<<<grid, block, smem, s>>>(args...) with the programmatic-stream-
+// serialization attribute (captured into graphs as programmatic edges)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 }  // namespace tvb

@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(kRestrictThreads) k_restrict(Agglo A, const ui
                                                                const double* __restrict__ y,
                                                                const double* __restrict__ y2, const SolverState* st,
                                                                double* yc, const int* stop) {
+  pdl_entry();
   __shared__ double red[6 * (kRestrictThreads / 32)], m[6];
   if (stop != nullptr && *stop) return;
   const double beta = (y2 != nullptr) ? st->beta : 0.0;  // restrict y + beta*y2
@@ -318,6 +319,7 @@ __global__ void __launch_bounds__(kRestrictWarpThreads) k_restrict_warp(Agglo A,
                                                                         const double* __restrict__ y2,
                                                                         const SolverState* st, double* yc,
                                                                         const int* stop) {
+  pdl_entry();
   if (stop != nullptr && *stop) return;
   const int lane = threadIdx.x & 31;
   const long long B = (long long)blockIdx.x * (kRestrictWarpThreads / 32) + (threadIdx.x >> 5);
@@ -402,21 +404,22 @@ cudaError_t launch_restrict(const Agglo& A, const uint8_t* nflags, DeflData D, c
   const bool warp = mode == 1 || (mode == 0 && A.b < 8);
   if (warp) {
     const unsigned gw = (unsigned)((A.nb + 7) / 8);
-    if (A.b == 8) k_restrict_warp<8><<<gw, kRestrictWarpThreads, 0, s>>>(A, nflags, D, y, y2, st, yc, stop);
-    else if (A.b == 4) k_restrict_warp<4><<<gw, kRestrictWarpThreads, 0, s>>>(A, nflags, D, y, y2, st, yc, stop);
-    else k_restrict_warp<0><<<gw, kRestrictWarpThreads, 0, s>>>(A, nflags, D, y, y2, st, yc, stop);
+    if (A.b == 8) launch_k(k_restrict_warp<8>, gw, kRestrictWarpThreads, 0, s, A, nflags, D, y, y2, st, yc, stop);
+    else if (A.b == 4) launch_k(k_restrict_warp<4>, gw, kRestrictWarpThreads, 0, s, A, nflags, D, y, y2, st, yc, stop);
+    else launch_k(k_restrict_warp<0>, gw, kRestrictWarpThreads, 0, s, A, nflags, D, y, y2, st, yc, stop);
     return cudaGetLastError();
   }
   const unsigned g = (unsigned)A.nb;
-  if (A.b == 8) k_restrict<8><<<g, kRestrictThreads, 0, s>>>(A, nflags, D, y, y2, st, yc, stop);
-  else if (A.b == 4) k_restrict<4><<<g, kRestrictThreads, 0, s>>>(A, nflags, D, y, y2, st, yc, stop);
-  else k_restrict<0><<<g, kRestrictThreads, 0, s>>>(A, nflags, D, y, y2, st, yc, stop);
+  if (A.b == 8) launch_k(k_restrict<8>, g, kRestrictThreads, 0, s, A, nflags, D, y, y2, st, yc, stop);
+  else if (A.b == 4) launch_k(k_restrict<4>, g, kRestrictThreads, 0, s, A, nflags, D, y, y2, st, yc, stop);
+  else launch_k(k_restrict<0>, g, kRestrictThreads, 0, s, A, nflags, D, y, y2, st, yc, stop);
   return cudaGetLastError();
 }
 
 // nu_B = S_B mu_B
 __global__ void k_block_nu(long long nb, const double* S, const int* perm, const double* mu, double* nu,
                            const int* stop) {
+  pdl_entry();
   if (stop != nullptr && *stop) return;
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= 6 * nb) return;
@@ -430,7 +433,7 @@ __global__ void k_block_nu(long long nb, const double* S, const int* perm, const
 
 cudaError_t launch_block_nu(const Agglo& A, DeflData D, const double* mu, double* nu, cudaStream_t s,
                             const int* stop) {
-  k_block_nu<<<(unsigned)((6 * A.nb + 255) / 256), 256, 0, s>>>(A.nb, D.S, D.perm, mu, nu, stop);
+  launch_k(k_block_nu, (unsigned)((6 * A.nb + 255) / 256), 256, 0, s, A.nb, D.S, D.perm, mu, nu, stop);
   return cudaGetLastError();
 }
 
@@ -447,6 +450,7 @@ __global__ void __launch_bounds__(kProlongThreads) k_prolong(Agglo A, const uint
                                                  const double* __restrict__ cen, const double* __restrict__ nu,
                                                  double* __restrict__ out, const double* __restrict__ z,
                                                  double* __restrict__ x, const SolverState* st, int mode) {
+  pdl_entry();
   const Grid& G = A.g;
   const unsigned n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= (unsigned)G.nn) return;
@@ -509,9 +513,9 @@ cudaError_t launch_prolong(const Agglo& A, const uint8_t* nflags, DeflData D, co
                            const double* z, const void* state, int mode, cudaStream_t s, double* x) {
   const unsigned g = (unsigned)((A.g.nn + kProlongThreads - 1) / kProlongThreads);
   const SolverState* st = (const SolverState*)state;
-  if (A.b == 8) k_prolong<8><<<g, kProlongThreads, 0, s>>>(A, nflags, D.cen, nu, out, z, x, st, mode);
-  else if (A.b == 4) k_prolong<4><<<g, kProlongThreads, 0, s>>>(A, nflags, D.cen, nu, out, z, x, st, mode);
-  else k_prolong<0><<<g, kProlongThreads, 0, s>>>(A, nflags, D.cen, nu, out, z, x, st, mode);
+  if (A.b == 8) launch_k(k_prolong<8>, g, kProlongThreads, 0, s, A, nflags, D.cen, nu, out, z, x, st, mode);
+  else if (A.b == 4) launch_k(k_prolong<4>, g, kProlongThreads, 0, s, A, nflags, D.cen, nu, out, z, x, st, mode);
+  else launch_k(k_prolong<0>, g, kProlongThreads, 0, s, A, nflags, D.cen, nu, out, z, x, st, mode);
   return cudaGetLastError();
 }
 

@@ -119,6 +119,7 @@ constexpr int kRing = kAhead + 1;
 //   plane k through shared memory; the owner thread finishes the node.
 template <int NT, int MINB, bool DOT, bool MASKOUT>
 __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
+  pdl_entry();
   extern __shared__ double smem[];
   if (P.stop != nullptr && *P.stop) return;
   const Grid& G = P.g;
@@ -412,10 +413,10 @@ static void set_smem_attr(size_t bytes) {
 template <int NT, int MINB>
 static void launch_nt(dim3 grid, size_t smem, cudaStream_t s, const MatvecParams& P, const Modal& M) {
   const bool dot = P.dot_partial != nullptr, mo = P.mask_out && P.fixed != nullptr;
-  if (dot && mo) k_matvec<NT, MINB, true, true><<<grid, NT, smem, s>>>(P, M);
-  else if (dot) k_matvec<NT, MINB, true, false><<<grid, NT, smem, s>>>(P, M);
-  else if (mo) k_matvec<NT, MINB, false, true><<<grid, NT, smem, s>>>(P, M);
-  else k_matvec<NT, MINB, false, false><<<grid, NT, smem, s>>>(P, M);
+  if (dot && mo) launch_k(k_matvec<NT, MINB, true, true>, grid, NT, smem, s, P, M);
+  else if (dot) launch_k(k_matvec<NT, MINB, true, false>, grid, NT, smem, s, P, M);
+  else if (mo) launch_k(k_matvec<NT, MINB, false, true>, grid, NT, smem, s, P, M);
+  else launch_k(k_matvec<NT, MINB, false, false>, grid, NT, smem, s, P, M);
 }
 
 cudaError_t launch_matvec(const MatvecPlan& pl, MatvecParams P, const Modal& M, cudaStream_t s) {

@@ -37,6 +37,7 @@ namespace tvb {
 template <int MC>
 __global__ void k_dense_gemv(long long nc, const double* Einv, const double* yc, long long ldy, double* mu,
                             long long ldm, const int* stop, long long stop_ld) {
+  pdl_entry();
   if (stop != nullptr) {
     bool all = true;
 #pragma unroll
@@ -72,10 +73,10 @@ cudaError_t launch_dense_gemv_multi(long long nc, const double* Einv, int ncols,
     double* m = mu + c0 * ldm;
     const int* st = stop ? stop + c0 * stop_ld : nullptr;
     switch (k) {
-      case 1: k_dense_gemv<1><<<grid, 256, 0, s>>>(nc, Einv, y, ldy, m, ldm, st, stop_ld); break;
-      case 2: k_dense_gemv<2><<<grid, 256, 0, s>>>(nc, Einv, y, ldy, m, ldm, st, stop_ld); break;
-      case 3: k_dense_gemv<3><<<grid, 256, 0, s>>>(nc, Einv, y, ldy, m, ldm, st, stop_ld); break;
-      default: k_dense_gemv<4><<<grid, 256, 0, s>>>(nc, Einv, y, ldy, m, ldm, st, stop_ld); break;
+      case 1: launch_k(k_dense_gemv<1>, grid, 256, 0, s, nc, Einv, y, ldy, m, ldm, st, stop_ld); break;
+      case 2: launch_k(k_dense_gemv<2>, grid, 256, 0, s, nc, Einv, y, ldy, m, ldm, st, stop_ld); break;
+      case 3: launch_k(k_dense_gemv<3>, grid, 256, 0, s, nc, Einv, y, ldy, m, ldm, st, stop_ld); break;
+      default: launch_k(k_dense_gemv<4>, grid, 256, 0, s, nc, Einv, y, ldy, m, ldm, st, stop_ld); break;
     }
   }
   return cudaGetLastError();

@@ -130,27 +130,57 @@ __global__ void k_pcg_update(long long n, double* x, double* r, double* z, const
   });
 }
 
-// Same update, 16-byte vector accesses (all six vectors 16-byte aligned): each
-// thread streams two double2 of every vector per step, so ~12 independent
-// 16-byte loads are in flight per thread. Identical arithmetic per element;
-// the partial sums run in a different (still fixed) order.
-// WX = false: x is not touched (the deflated solver folds x += alpha p into
-// the prolongation, which reads p anyway).
+// Same update, 16-byte vector accesses (all six vectors 16-byte aligned),
+// grid-strided so that all CTAs sweep the vectors together. Identical
+// arithmetic per element; the partial sums run in a different (still fixed)
+// order. WX = false: x is not touched (the deflated solver folds x += alpha p
+// into the prolongation, which reads p anyway).
 template <bool WX>
 __global__ void __launch_bounds__(256) k_pcg_update_v2(long long n, double* __restrict__ x, double* __restrict__ r,
                                                        double* __restrict__ z, const double* __restrict__ p,
                                                        const double* __restrict__ q,
                                                        const double* __restrict__ inv_d, SolverState* st,
                                                        double* partials, const double* pq_parts, int n_parts) {
+  pdl_entry();
   __shared__ double red[32];
   __shared__ double s_pq;
   if (st->done) return;
+  const long long n2 = n >> 1;
+  const long long hi = n2;  // grid-strided: all CTAs sweep the vectors together
+  double2* x2 = reinterpret_cast<double2*>(x);
+  double2* r2 = reinterpret_cast<double2*>(r);
+  double2* z2 = reinterpret_cast<double2*>(z);
+  const double2* p2 = reinterpret_cast<const double2*>(p);
+  const double2* q2 = reinterpret_cast<const double2*>(q);
+  const double2* d2 = reinterpret_cast<const double2*>(inv_d);
+  // Software pipeline over pairs (i, i + blockDim.x), i += 2 * blockDim.x:
+  // the operands of pair k+1 are loaded before pair k is processed, and the
+  // first pair's loads are issued before the p.q reduction so their DRAM
+  // latency overlaps the partial-sum reads. Same elements in the same order
+  // per thread as a plain loop (bitwise identical partial sums).
+  struct Ops {
+    double2 p, x, q, r, d;
+  };
+  auto load = [&](long long k, Ops& o) {
+    if (WX) {
+      o.p = p2[k];
+      o.x = x2[k];
+    }
+    o.q = q2[k];
+    o.r = r2[k];
+    o.d = __ldg(d2 + k);
+  };
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long step = (long long)gridDim.x * blockDim.x;
+  Ops a{}, b{};
+  if (i < hi) load(i, a);
+  if (i + step < hi) load(i + step, b);
   // p.q from the matvec's per-CTA partials, summed by every CTA in the same
   // fixed order (replaces a separate finaliser launch)
   if (pq_parts != nullptr) {
     if (threadIdx.x < 32) {
       double s = 0.0;
-      for (int i = threadIdx.x; i < n_parts; i += 32) s += __ldcg(pq_parts + i);
+      for (int j = threadIdx.x; j < n_parts; j += 32) s += __ldcg(pq_parts + j);
       s = warp_sum(s);
       if (threadIdx.x == 0) s_pq = s;
     }
@@ -161,45 +191,38 @@ __global__ void __launch_bounds__(256) k_pcg_update_v2(long long n, double* __re
   __syncthreads();
   const double pq = s_pq;
   const double alpha = st->rz / pq;
-  const long long n2 = n >> 1;
-  const long long per = (n2 + gridDim.x - 1) / gridDim.x;
-  const long long lo = blockIdx.x * per, hi = min(n2, lo + per);
-  double2* x2 = reinterpret_cast<double2*>(x);
-  double2* r2 = reinterpret_cast<double2*>(r);
-  double2* z2 = reinterpret_cast<double2*>(z);
-  const double2* p2 = reinterpret_cast<const double2*>(p);
-  const double2* q2 = reinterpret_cast<const double2*>(q);
-  const double2* d2 = reinterpret_cast<const double2*>(inv_d);
   double rr = 0.0, rz = 0.0;
-  auto one = [&](double2 pi, double2 xi, double2 qi, double2 ri, double2 di, long long i) {
+  auto one = [&](const Ops& o, long long k) {
     if (WX) {
-      xi.x = fma(alpha, pi.x, xi.x);
-      xi.y = fma(alpha, pi.y, xi.y);
-      __stcs(x2 + i, xi);  // x and r are next read one iteration later: evict first
+      double2 xi = o.x;
+      xi.x = fma(alpha, o.p.x, xi.x);
+      xi.y = fma(alpha, o.p.y, xi.y);
+      __stcs(x2 + k, xi);  // x and r are next read one iteration later: evict first
     }
-    ri.x = fma(-alpha, qi.x, ri.x);
-    ri.y = fma(-alpha, qi.y, ri.y);
+    double2 ri = o.r;
+    ri.x = fma(-alpha, o.q.x, ri.x);
+    ri.y = fma(-alpha, o.q.y, ri.y);
     double2 zi;
-    zi.x = di.x * ri.x;
-    zi.y = di.y * ri.y;
-    __stcs(r2 + i, ri);
-    z2[i] = zi;
+    zi.x = o.d.x * ri.x;
+    zi.y = o.d.y * ri.y;
+    __stcs(r2 + k, ri);
+    z2[k] = zi;
     rr = fma(ri.x, ri.x, rr);
     rz = fma(ri.x, zi.x, rz);
     rr = fma(ri.y, ri.y, rr);
     rz = fma(ri.y, zi.y, rz);
   };
-  long long i = lo + threadIdx.x;
-  for (; i + blockDim.x < hi; i += 2 * blockDim.x) {
-    const long long j = i + blockDim.x;
-    const double2 pa = WX ? p2[i] : double2{}, pb = WX ? p2[j] : double2{};
-    const double2 xa = WX ? x2[i] : double2{}, xb = WX ? x2[j] : double2{};
-    const double2 qa = q2[i], qb = q2[j], ra = r2[i], rb = r2[j];
-    const double2 da = __ldg(d2 + i), db = __ldg(d2 + j);
-    one(pa, xa, qa, ra, da, i);
-    one(pb, xb, qb, rb, db, j);
+  while (i < hi) {
+    const long long inext = i + 2 * step;
+    Ops na{}, nb{};
+    if (inext < hi) load(inext, na);
+    if (inext + step < hi) load(inext + step, nb);
+    one(a, i);
+    if (i + step < hi) one(b, i + step);
+    a = na;
+    b = nb;
+    i = inext;
   }
-  if (i < hi) one(WX ? p2[i] : double2{}, WX ? x2[i] : double2{}, q2[i], r2[i], __ldg(d2 + i), i);
   if ((n & 1) && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {  // odd tail element
     const long long k = n - 1;
     if (WX) x[k] = fma(alpha, p[k], x[k]);
@@ -246,6 +269,7 @@ cudaError_t launch_x_finish(long long n, double* x, const double* p, const Solve
 
 // plain PCG direction update p = z + beta p
 __global__ void k_pcg_pupdate(long long n, double* p, const double* z, const SolverState* st) {
+  pdl_entry();
   if (st->done) return;
   const double beta = st->beta;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -348,9 +372,11 @@ cudaError_t launch_pcg_update(long long n, double* x, double* r, double* z, cons
   const bool vec16 = (((x ? reinterpret_cast<uintptr_t>(x) : 0) | reinterpret_cast<uintptr_t>(r) |
                        reinterpret_cast<uintptr_t>(z) | reinterpret_cast<uintptr_t>(p) |
                        reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(inv_d)) & 15) == 0;
-  // grid: at most 4 CTAs per SM, an exact multiple of the SM count for large
-  // vectors (C4: 774 -> 592 CTAs, 218.3 -> 213 us per DPCG iteration; 8 and
-  // 2 per SM were slower); TVB_UPD_CTAS overrides (A/B experiments)
+  // grid: at most 2 CTAs per SM (an exact multiple of the SM count for large
+  // vectors). Measured with the grid-strided prefetching kernel: C4 203.7 us
+  // per DPCG iteration (592 CTAs: 207.7; the previous contiguous-range kernel
+  // at 592 CTAs: 204.5), C3 111.8 (116.3), C5 1584 (1600); TVB_UPD_CTAS
+  // overrides (A/B experiments)
   static int upd_ctas = -1;
   if (upd_ctas < 0) {
     upd_ctas = getenv("TVB_UPD_CTAS") ? atoi(getenv("TVB_UPD_CTAS")) : 0;
@@ -358,14 +384,14 @@ cudaError_t launch_pcg_update(long long n, double* x, double* r, double* z, cons
       int dev = 0, nsm = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-      upd_ctas = 4 * nsm;
+      upd_ctas = 2 * nsm;
     }
   }
   const int g = std::min(std::min(upd_ctas, kMaxReduceCtas), reduce_grid(n));
   if (vec16 && x != nullptr) {
-    k_pcg_update_v2<true><<<g, 256, 0, s>>>(n, x, r, z, p, q, inv_d, st, partials, pq_parts, n_parts);
+    launch_k(k_pcg_update_v2<true>, g, 256, 0, s, n, x, r, z, p, q, inv_d, st, partials, pq_parts, n_parts);
   } else if (vec16) {
-    k_pcg_update_v2<false><<<g, 256, 0, s>>>(n, x, r, z, p, q, inv_d, st, partials, pq_parts, n_parts);
+    launch_k(k_pcg_update_v2<false>, g, 256, 0, s, n, x, r, z, p, q, inv_d, st, partials, pq_parts, n_parts);
   } else {
     if (pq_parts != nullptr) k_finalize_pq<<<1, 256, 0, s>>>(pq_parts, n_parts, st);
     k_pcg_update<<<reduce_grid(n), 256, 0, s>>>(n, x, r, z, p, q, inv_d, st, partials);
@@ -374,7 +400,7 @@ cudaError_t launch_pcg_update(long long n, double* x, double* r, double* z, cons
 }
 
 cudaError_t launch_pcg_pupdate(long long n, double* p, const double* z, const SolverState* st, cudaStream_t s) {
-  k_pcg_pupdate<<<reduce_grid(n) * 4, 256, 0, s>>>(n, p, z, st);
+  launch_k(k_pcg_pupdate, reduce_grid(n) * 4, 256, 0, s, n, p, z, st);
   return cudaGetLastError();
 }
 
