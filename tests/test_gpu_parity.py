@@ -205,6 +205,28 @@ def test_dpcg_c1_golden(tv, golden, coarse):
     assert abs(rp.iterations - int(golden["c1_plain_t8_iters"])) <= 1
 
 
+def test_dpcg_c3_c4_survey_kats(tv):
+    """BASELINE configs[2] (C3, 80x40x40, b = 4) and the C4 geometry (160x80x80,
+    b = 8), full solid, point load at the x = nx face centre: the reference's
+    own measurements (SURVEY.md 8c KAT table / 8a a8 row): C3 J0 =
+    2.4345313102 with 253 DPCG and 503 plain-PCG iterations; C4 geometry 447
+    DPCG and 991 plain-PCG iterations (tol 1e-8)."""
+    from paper_2203_15115_b200 import fea
+
+    for dims, b, J0, it_d, it_p in (((80, 40, 40), 4, 2.4345313102, 253, 503), ((160, 80, 80), 8, None, 447, 991)):
+        nx, ny, nz = dims
+        c = (nx, ny // 2, nz // 2)
+        d, case, fixed, f = cantilever(nx, ny, nz, c, c)
+        op = make_op(tv, dims, np.ones(d.n_elems), fixed)
+        defl = fea.build_deflation(d, op.topology, fixed, b)
+        r = fea.solve_static(op, f, tol=1e-8, deflation=defl)
+        assert abs(r.iterations - it_d) <= 1, (dims, r.iterations)
+        if J0 is not None:
+            assert float(f @ r.u) == pytest.approx(J0, rel=1e-9)  # J0 pinned to 11 digits
+        rp = fea.solve_static(op, f, tol=1e-8)
+        assert abs(rp.iterations - it_p) <= 1, (dims, rp.iterations)
+
+
 def test_solver_edge_cases(tv, golden):
     from paper_2203_15115_b200 import fea
     from paper_2203_15115_b200.errors import DimensionMismatch, NoConvergence
