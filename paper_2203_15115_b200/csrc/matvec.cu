@@ -224,12 +224,14 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
       if (k >= 0 && k < G.pz) {
         const char* src = reinterpret_cast<const char*>(P.u + plane_stride * k);
         const unsigned base = up_s + (unsigned)(8 * sl * PS);
+        // all list entries first (unused slots are read but never followed),
+        // then the predicated copies: no LDS -> LDGSTS pairs in the stream
+        int2 e[kStage];
+#pragma unroll
+        for (int q = 0; q < kStage; ++q) e[q] = st_list[q * NT + t];
 #pragma unroll
         for (int q = 0; q < kStage; ++q)
-          if (q < ncnt) {
-            const int2 e = st_list[q * NT + t];
-            cp_async8_s(base + (unsigned)e.x, src + e.y);
-          }
+          if (q < ncnt) cp_async8_s(base + (unsigned)e[q].x, src + e[q].y);
       } else {  // halo plane above / below the grid (first / last piece only)
         double* dst = Up + sl * PS;
 #pragma unroll
@@ -258,6 +260,9 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
     const long long own_node = G.node(min(x0 + tx, G.px - 1), min(y0 + ty, G.py - 1), kz0);
     double* yrow = P.y + 3 * own_node;
     const uint8_t* frow = MASKOUT ? P.fixed + own_node : nullptr;
+    // fixed-DOF flags of the owned node, loaded one output plane ahead (the
+    // byte load's latency is covered by a whole z-step)
+    uint8_t fnext = (MASKOUT && owner && kz0 < kz1) ? *frow : (uint8_t)0;
 
     // sk = ring slot of plane / layer k; plane k+1 sits in sk+1, plane k+kAhead in sk-1 (mod kRing)
     auto step = [&](int k, int sk, const double (&bot)[12], double (&top)[12]) {
@@ -311,7 +316,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
   #pragma unroll
         for (int a = 0; a < 3; ++a) v[a] = ((face[9 + a] + e10[6 + a]) + e01[3 + a]) + e11[a];
         if (owner) {
-          const uint8_t fx = MASKOUT ? *frow : 0;
+          const uint8_t fx = MASKOUT ? fnext : 0;
   #pragma unroll
           for (int a = 0; a < 3; ++a) {
             double w = ((fx >> a) & 1) ? 0.0 : v[a];
@@ -321,7 +326,10 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
           }
         }
         yrow += plane_stride;
-        if (MASKOUT) frow += (long long)G.px * G.py;
+        if (MASKOUT) {
+          frow += (long long)G.px * G.py;
+          if (owner && k + 1 < kz1) fnext = *frow;
+        }
       }
     };
 
