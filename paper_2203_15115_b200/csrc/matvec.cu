@@ -107,6 +107,9 @@ __device__ __forceinline__ void xy_inverse(double (&f)[12]) {
 
 constexpr int kStage = 4;   // max staged node-plane doubles per thread ((wy+1)*3(wx+1) <= kStage*NT)
 constexpr int kXcPad = 64;  // exchange rows past NT read (harmlessly) by edge threads
+// doubles per thread slot of the face exchange (9 used): 80-byte slots keep
+// every 16-byte access aligned and a quarter-warp of them bank-conflict free
+constexpr int kXw = 10;
 constexpr int kAhead = 4;   // node planes in flight ahead of the compute (cp.async groups)
 constexpr int kRing = kAhead + 1;
 
@@ -133,8 +136,8 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
 
   double* Up = smem;                  // [kRing][PS] node plane ring
   double* Oc = Up + kRing * PS;       // [kRing][OS] occupancy layer ring
-  double* Xc = Oc + kRing * OS;       // [2][NT + kXcPad][9] face exchange
-  const int XS = 9 * (NT + kXcPad);
+  double* Xc = smem + ((kRing * PS + kRing * OS + 1) & ~1);  // [2][NT + kXcPad][kXw] face exchange (16-B aligned)
+  const int XS = kXw * (NT + kXcPad);
   double* red = Xc + 2 * XS;
   // [kStage][NT] staging lists: (smem byte offset, in-plane global byte offset)
   int2* st_list = reinterpret_cast<int2*>(red + NT / 32 + 1);
@@ -293,8 +296,11 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
       double* xs = Xc + (k & 1) * XS;
       if (out) {
         xy_inverse(face);
+        // nodes (0,0), (1,0), (0,1): four 16-byte stores and one 8-byte
+        double2* x2 = reinterpret_cast<double2*>(xs + kXw * t);
   #pragma unroll
-        for (int i = 0; i < 9; ++i) xs[9 * t + i] = face[i];  // nodes (0,0), (1,0), (0,1)
+        for (int i = 0; i < 4; ++i) x2[i] = make_double2(face[2 * i], face[2 * i + 1]);
+        xs[kXw * t + 8] = face[8];
       }
       // dot epilogue operand: u at the owned node, read from staged plane k
       // BEFORE the barrier (after it, a faster thread may already refill the
@@ -309,12 +315,16 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
       if (out) {
         // node (x0+tx, y0+ty) = local (1,1) of this column, (0,1) of column
         // tx+1, (1,0) of column ty+1 and (0,0) of column (tx+1, ty+1).
-        const double* e10 = xs + 9 * (t + 1);
-        const double* e01 = xs + 9 * (t + wx);
-        const double* e11 = xs + 9 * (t + wx + 1);
+        const double* e10 = xs + kXw * (t + 1);
+        const double* e01 = xs + kXw * (t + wx);
+        const double* e11 = xs + kXw * (t + wx + 1);
+        const double2 a67 = *reinterpret_cast<const double2*>(e10 + 6);
+        const double2 b45 = *reinterpret_cast<const double2*>(e01 + 4);
+        const double2 c01 = *reinterpret_cast<const double2*>(e11);
+        const double n10[3] = {a67.x, a67.y, e10[8]}, n01[3] = {e01[3], b45.x, b45.y}, n11[3] = {c01.x, c01.y, e11[2]};
         double v[3];
   #pragma unroll
-        for (int a = 0; a < 3; ++a) v[a] = ((face[9 + a] + e10[6 + a]) + e01[3 + a]) + e11[a];
+        for (int a = 0; a < 3; ++a) v[a] = ((face[9 + a] + n10[a]) + n01[a]) + n11[a];
         if (owner) {
           const uint8_t fx = MASKOUT ? fnext : 0;
   #pragma unroll
@@ -361,7 +371,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
 
 static size_t matvec_smem(int nt, int wx, int wy) {
   const int PS = (wy + 1) * plane_row_stride(wx);
-  return sizeof(double) * (kRing * (size_t)PS + kRing * (size_t)wx * wy + 2 * 9 * (size_t)(nt + kXcPad) + nt / 32 + 1) +
+  return sizeof(double) * (kRing * (size_t)PS + kRing * (size_t)wx * wy + 1 + 2 * kXw * (size_t)(nt + kXcPad) + nt / 32 + 1) +
          2 * sizeof(int) * kStage * (size_t)nt;
 }
 
