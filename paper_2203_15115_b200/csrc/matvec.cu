@@ -296,11 +296,12 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
       double* xs = Xc + (k & 1) * XS;
       if (out) {
         xy_inverse(face);
-        // nodes (0,0), (1,0), (0,1): four 16-byte stores and one 8-byte
+        // nodes (0,0), (1,0), (0,1): five 16-byte stores (slot word 9 unused);
+        // 8-byte accesses at an 80-byte stride would conflict 2-way
         double2* x2 = reinterpret_cast<double2*>(xs + kXw * t);
   #pragma unroll
         for (int i = 0; i < 4; ++i) x2[i] = make_double2(face[2 * i], face[2 * i + 1]);
-        xs[kXw * t + 8] = face[8];
+        x2[4] = make_double2(face[8], 0.0);
       }
       // dot epilogue operand: u at the owned node, read from staged plane k
       // BEFORE the barrier (after it, a faster thread may already refill the
@@ -319,9 +320,12 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
         const double* e01 = xs + kXw * (t + wx);
         const double* e11 = xs + kXw * (t + wx + 1);
         const double2 a67 = *reinterpret_cast<const double2*>(e10 + 6);
+        const double2 a89 = *reinterpret_cast<const double2*>(e10 + 8);
+        const double2 b23 = *reinterpret_cast<const double2*>(e01 + 2);
         const double2 b45 = *reinterpret_cast<const double2*>(e01 + 4);
         const double2 c01 = *reinterpret_cast<const double2*>(e11);
-        const double n10[3] = {a67.x, a67.y, e10[8]}, n01[3] = {e01[3], b45.x, b45.y}, n11[3] = {c01.x, c01.y, e11[2]};
+        const double2 c23 = *reinterpret_cast<const double2*>(e11 + 2);
+        const double n10[3] = {a67.x, a67.y, a89.x}, n01[3] = {b23.y, b45.x, b45.y}, n11[3] = {c01.x, c01.y, c23.x};
         double v[3];
   #pragma unroll
         for (int a = 0; a < 3; ++a) v[a] = ((face[9 + a] + n10[a]) + n01[a]) + n11[a];
