@@ -367,11 +367,14 @@ def dpcg_roofline(d, defl, us_per_iter, p64, hbm):
 
 
 def secondary_solves(tv, fea, torch, p64, hbm):
-    """Deflated PCG solves (device-timed): C1, the C4 geometry (north-star target)
-    and C2(b) (BASELINE configs[1] part b; infeasible for the reference)."""
+    """Deflated PCG solves (device-timed): C1, C3, the C4 geometry (north-star
+    target), C5 (load case 1: 5x5 patch) and C2(b) (BASELINE configs[1] part
+    b; C2(b) and C5 are infeasible for the reference's dense coarse factor)."""
     out = {}
     specs = [("C1_40x20x20_b4", (40, 20, 20), 4, (40, 10, 10), (40, 10, 10), None),
+             ("C3_80x40x40_b4", (80, 40, 40), 4, (80, 20, 20), (80, 20, 20), None),
              ("C4a_160x80x80_b8", (160, 80, 80), 8, (160, 39, 39), (160, 41, 41), None),
+             ("C5_320x160x160_b8", (320, 160, 160), 8, (320, 78, 78), (320, 82, 82), None),
              ("C2b_128^3_b4_bernoulli", (128, 128, 128), 4, None, None, "c2b")]
     for name, dims, b, lo, hi, kind in specs:
         try:
