@@ -486,15 +486,17 @@ int pcg_solve_multi(const PcgProblem& P, PcgResult* R, int* rstat, cudaStream_t 
   int batch = P.check_every > 0 ? P.check_every : 8;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
-  // Whole-solve graph (default): a conditional WHILE node whose body holds
+  // Whole-solve graph (TVB_GRAPH_WHILE=1): a conditional WHILE node whose body holds
   // `check_every` iterations (TVB_WHILE_BODY overrides) and a one-thread
   // kernel that re-arms the condition while any RHS is running, so the
   // iteration loop never returns to the host (no per-batch launch + state
   // read-back + synchronise). Measured within noise of the host loop at C1-C4
   // (the per-batch round trips were already hidden), 1 % faster for the 2-RHS
   // C4 batch; bodies of 4-8 iterations beat 1-2 (C1 5.64 vs 6.04 ms per solve).
-  // TVB_GRAPH_WHILE=0: graphs of `check_every` iterations from a host loop.
-  static const int while_env = getenv("TVB_GRAPH_WHILE") ? atoi(getenv("TVB_GRAPH_WHILE")) : 1;
+  // Not the default: kernels inside conditional bodies are invisible to the
+  // ncu launch lists (profiles/) and per-kernel tracing, for no measured gain.
+  // Default: graphs of `check_every` iterations launched from a host loop.
+  static const int while_env = getenv("TVB_GRAPH_WHILE") ? atoi(getenv("TVB_GRAPH_WHILE")) : 0;
   const bool use_while = while_env != 0;
   if (use_while) {
     static const int body_env = getenv("TVB_WHILE_BODY") ? atoi(getenv("TVB_WHILE_BODY")) : 0;

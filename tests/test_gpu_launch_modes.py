@@ -59,7 +59,7 @@ def test_launch_modes_bitwise():
     base = _run({})
     assert base["it"] > 10
     assert base["bu"][0] == base["u"] and base["bit"][0] == base["it"]  # batch column 0 == single solve
-    for extra in ({"TVB_PDL": "0"}, {"TVB_GRAPH_WHILE": "0"}, {"TVB_GRAPH_WHILE": "5"}):
+    for extra in ({"TVB_PDL": "0"}, {"TVB_GRAPH_WHILE": "1"}, {"TVB_GRAPH_WHILE": "1", "TVB_WHILE_BODY": "3"}):
         other = _run(extra)
         assert other == base, (extra, other, base)
     assert np.isfinite(base["J"])
