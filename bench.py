@@ -84,13 +84,18 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(name: str):
-    """DRAM bytes per launch of the matvec from the committed ncu summary."""
+def ncu_traffic(*names: str):
+    """DRAM bytes per launch of the matvec from the committed ncu summary
+    (the first of `names` present: the latest capture first)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
-            return json.load(fh).get(name, {}).get("dram_bytes_per_launch")
+            d = json.load(fh)
+        for name in names:
+            if name in d:
+                return d[name].get("dram_bytes_per_launch")
     except Exception:
-        return None
+        pass
+    return None
 
 
 class ClockSampler:
@@ -302,7 +307,7 @@ def main():
                    "parallelism": f"replicas x{world}"},
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": ncu_traffic("k_matvec_c2"), "peak_kind": peak_kind,
+            "traffic": ncu_traffic("k_matvec_c2_r01c", "k_matvec_c2_r01b", "k_matvec_c2"), "peak_kind": peak_kind,
             "alg_bytes_per_launch": alg_bytes,
             "note": "mode-space kernel: ~150 fp64 ops/element, so its own bound is HBM",
             "north_star": {"definition": "max(1152*Ne FMA-flops / P64, bytes / HBM)", "p64_tflops_live": p64,
