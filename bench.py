@@ -34,6 +34,13 @@ sys.path.insert(0, ROOT)
 
 N_C2 = 128
 METRIC = "hex matvec GDOF/s"
+# the workload both arms report (identical dict, so the driver sees the same config)
+CONFIG = {"workload": "C2(a) 128^3 Bernoulli(0.7) K.u (BASELINE configs[1])", "n": N_C2,
+          "n_dofs": 3 * (N_C2 + 1) ** 3, "n_elems": N_C2 ** 3, "parallelism": "replicas (one per GPU)"}
+# fp64 operations per element the mode-space matvec executes (csrc/matvec.cu:
+# xy forward 24, z butterfly 24, occupancy scaling 8, mode operator 33, z
+# inverse + carry 36, xy inverse 24, four-way node sum 9): its own issue bound
+MATVEC_FP64_OPS = 158
 
 
 def parse(argv=None):
@@ -175,7 +182,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": base["value"], "unit": "GDOF/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2(a) 128^3 Bernoulli(0.7) K.u", "n": N_C2},
+        "config": dict(CONFIG),
         "cpu_baseline": base,
         "e2e": {"value": base["value"], "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -263,6 +270,9 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     t_total = max_over_ranks(float(times_ms.sum()) / 1e3, device="cuda")
+    step_stats = {"mean_ms": float(times_ms.mean()), "median_ms": float(np.median(times_ms)),
+                  "p10_ms": float(np.percentile(times_ms, 10)), "p90_ms": float(np.percentile(times_ms, 90)),
+                  "min_ms": float(times_ms.min()), "max_ms": float(times_ms.max())}
     nd, ne = d.n_dofs, d.n_elems
     value = world * nd * args.steps / t_total / 1e9
     ms_per_step = t_total * 1e3 / args.steps
@@ -298,22 +308,32 @@ def main():
     achieved = alg_bytes / (ms_per_step / 1e3) / 1e9
     flops_dense = 1152.0 * ne
     t_star = max(flops_dense / (p64 * 1e12), alg_bytes / (hbm * 1e9)) if p64 > 0 else None
+    # the executed kernel's own bound: its bytes at HBM bandwidth vs its fp64
+    # instructions at the fp64 pipe rate (P64 counts an FMA as 2 flops, and a
+    # DADD / DMUL issues at the DFMA rate, so the op rate is P64 / 2)
+    t_hbm = alg_bytes / (hbm * 1e9)
+    t_fp64 = MATVEC_FP64_OPS * ne / (p64 / 2.0 * 1e12) if p64 > 0 else 0.0
+    t_own = max(t_hbm, t_fp64)
     line = {
         "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Bernoulli(0.7) occupancy, N(0,1) u)",
-        "config": {"workload": "C2(a) 128^3 Bernoulli(0.7) K.u (BASELINE configs[1])", "n": N_C2,
-                   "n_dofs": nd, "n_elems": ne, "l2": "flushed (512 MB write) before every timed step",
-                   "parallelism": f"replicas x{world}"},
+        "config": dict(CONFIG),
+        "l2": "flushed (512 MB write) before every timed step",
+        "step_stats": step_stats,
+        "value_median": nd / (step_stats["median_ms"] / 1e3) / 1e9 * world,
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": ncu_traffic("k_matvec_c2_r01c", "k_matvec_c2_r01b", "k_matvec_c2"), "peak_kind": peak_kind,
-            "alg_bytes_per_launch": alg_bytes,
-            "note": "mode-space kernel: ~150 fp64 ops/element, so its own bound is HBM",
-            "north_star": {"definition": "max(1152*Ne FMA-flops / P64, bytes / HBM)", "p64_tflops_live": p64,
+            "traffic": ncu_traffic("k_matvec_c2_r02", "k_matvec_c2_r01c", "k_matvec_c2_r01b", "k_matvec_c2"),
+            "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes,
+            "own_bound": {"t_hbm_us": t_hbm * 1e6, "t_fp64_issue_us": t_fp64 * 1e6,
+                          "fp64_ops_per_elem": MATVEC_FP64_OPS, "p64_tflops_live": p64,
+                          "frac": t_own / (ms_per_step / 1e3),
+                          "frac_median": t_own / (step_stats["median_ms"] / 1e3)},
+            "north_star": {"definition": "max(1152*Ne FMA-flops / P64, bytes / HBM) (dense-k0 flops the "
+                                         "mode-space kernel does not execute)",
                            "t_star_us": t_star * 1e6 if t_star else None,
-                           "frac": (t_star / (ms_per_step / 1e3)) if t_star else None,
-                           "dense_k0_equiv_tflops": flops_dense / (ms_per_step / 1e3) / 1e12},
+                           "frac": (t_star / (ms_per_step / 1e3)) if t_star else None},
         },
         "e2e": {"value": e2e_val, "unit": "GDOF/s", "h2d_bytes_per_step": 8 * nd, "d2h_bytes_per_step": 8 * nd,
                 "api": "StiffnessOperator.apply_host_batch (pinned host vectors, %d steps)" % e2e_steps,
@@ -325,6 +345,9 @@ def main():
         line["secondary"] = secondary_solves(tv, fea, torch, p64, hbm)
         line["secondary"]["C4_two_load_cases_batched"] = secondary_batch(tv, fea, torch, p64, hbm)
         line["secondary"]["C4_optimizer"] = secondary_optimizer(torch)
+        line["secondary"]["C4_fields"] = secondary_fields(tv, fea, torch, hbm)
+        if world == 1 and not args.no_cpu_baseline:
+            line["secondary"]["C1_optimizer"] = secondary_optimizer_c1(torch)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_matvec(occ, u)
@@ -415,11 +438,132 @@ def secondary_solves(tv, fea, torch, p64, hbm):
                          "n_coarse": defl.n_vectors,
                          "coarse": "nested dissection" if defl.nd is not None else "dense inverse",
                          "roofline": dpcg_roofline(d, defl, us_it, p64, hbm)}
+            if name.startswith("C1"):
+                # plain Jacobi PCG on the device, and the reference's CPU path
+                # (oracle port) for both solves, timed here on this box's cores
+                a.record()
+                rp = fea.solve_static(op, fd, tol=1e-8)
+                e.record()
+                torch.cuda.synchronize()
+                out[name]["plain"] = {"iterations": rp.iterations, "solve_ms": a.elapsed_time(e)}
+                out[name]["cpu"] = cpu_c1_solves(d, occ, fixed, f, setup + ms / 1e3, ms, a.elapsed_time(e))
             del op, defl, r
             torch.cuda.empty_cache()
         except Exception as exc:
             out[name] = {"error": repr(exc)[:300]}
     return out
+
+
+def cpu_c1_solves(d, occ, fixed, f, gpu_total_s, gpu_dpcg_ms, gpu_plain_ms):
+    """The reference's CPU path for the C1 solves (oracle port: numba kernels
+    restated in C with all host threads, scipy dense Cholesky coarse solve,
+    the reference's loop), timed in the same run on this box's host cores."""
+    try:
+        from oracle import topovox_oracle as O
+
+        O.build_lib()
+        ref = O.Operator(d.nx, d.ny, d.nz, d.h, occ, dirichlet=fixed)
+        t0 = time.perf_counter()
+        defl = O.Deflation(ref, 4)
+        defl.prepare()
+        t1 = time.perf_counter()
+        _, it, _ = O.solve_static(ref, f, tol=1e-8, deflation=defl)
+        t2 = time.perf_counter()
+        _, itp, _ = O.solve_static(ref, f, tol=1e-8)
+        t3 = time.perf_counter()
+        cores = O.lib().oracle_max_threads()
+        return {"kind": "port", "cores": cores,
+                "sample": f"C1 DPCG (b = 4, build + prepare + solve) and plain Jacobi PCG, tol 1e-8, {cores} threads",
+                "dpcg_setup_s": t1 - t0, "dpcg_solve_s": t2 - t1, "dpcg_iterations": it,
+                "plain_solve_s": t3 - t2, "plain_iterations": itp,
+                "speedup_dpcg_solve": (t2 - t1) / (gpu_dpcg_ms / 1e3),
+                "speedup_dpcg_with_setup": (t2 - t0) / gpu_total_s,
+                "speedup_plain": (t3 - t2) / (gpu_plain_ms / 1e3)}
+    except Exception as exc:  # pragma: no cover
+        return {"error": repr(exc)[:300]}
+
+
+def secondary_optimizer_c1(torch, outer=3):
+    """BASELINE configs[0] (C1) optimizer, first `outer` outer iterations, on
+    the device and on the reference's CPU path (the oracle's SPEC-restated
+    loop over the oracle FEA, all host threads) in the same run."""
+    try:
+        from oracle import topovox_oracle as O
+        from paper_2203_15115_b200 import optimize as opt
+        from paper_2203_15115_b200.mesh import assemble_force, dirichlet_dofs
+
+        prob = opt.cantilever_problem(40, 20, 20, (40, 10, 10), (40, 10, 10),
+                                      constraints=[opt.ConstraintSpec("compliance", 1.6)])
+        cfg = opt.OptimizerConfig(ersatz=1e-3, block=4, max_outer=outer)
+        opt.run(prob, opt.OptimizerConfig(ersatz=1e-3, block=4, max_outer=1))  # warm (graphs, plans)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, hist, _ = opt.run(prob, cfg)
+        torch.cuda.synchronize()
+        t_gpu = time.perf_counter() - t0
+        case = prob.load_cases[0]
+        fixed, f = dirichlet_dofs(prob.domain, case), assemble_force(prob.domain, case)
+        t0 = time.perf_counter()
+        _, hist_r, _ = O.run_optimizer(40, 20, 20, [(fixed, f)], [{"kind": "compliance", "alpha": 1.6, "case": 0}],
+                                       block=4, ersatz=1e-3, max_outer=outer)
+        t_cpu = time.perf_counter() - t0
+        return {"outer_iterations": len(hist), "gpu_s": t_gpu, "solves": sum(h.solves for h in hist),
+                "volumes": [round(h.v, 6) for h in hist], "volumes_oracle": [round(h["v"], 6) for h in hist_r],
+                "cpu": {"kind": "port", "cores": O.lib().oracle_max_threads(), "seconds": t_cpu,
+                        "sample": f"first {outer} outer iterations of the C1 run (base analysis included)"},
+                "speedup": t_cpu / t_gpu}
+    except Exception as exc:  # pragma: no cover
+        return {"error": repr(exc)[:300]}
+
+
+def secondary_fields(tv, fea, torch, hbm):
+    """Per-element sensitivity / level-set kernels at the C4 geometry
+    (160x80x80, full solid), device-timed (CUDA events, mean of 20 launches
+    after warm-up), each against its algorithmic HBM bytes (DESIGN.md §3,
+    SURVEY §8(d)): element state + T_J + p-norm sums 8 (N_d + 3 N_e); adjoint
+    right-hand side 8 (2 N_d + N_e); T_sigma 8 (2 N_d + 2 N_e); combine of two
+    fields (max-abs passes + weighted sum) 8 * 5 N_e; threshold select 16 N_e
+    (read the level set, write the occupancy)."""
+    try:
+        from paper_2203_15115_b200 import levelset, sensitivity
+
+        d = tv.Domain(160, 80, 80, 1.0)
+        case = _case(tv, d, (160, 39, 39), (160, 41, 41))
+        fixed = tv.dirichlet_dofs(d, case)
+        op = fea.StiffnessOperator(d, tv.Topology(d, np.ones(d.n_elems)), tv.Material(E=1.0, nu=0.3), fixed)
+        u = torch.from_numpy(np.random.default_rng(3).standard_normal(d.n_dofs)).cuda()
+        lam = torch.from_numpy(np.random.default_rng(4).standard_normal(d.n_dofs)).cuda()
+        nd, ne = d.n_dofs, d.n_elems
+        _, tj, sums = sensitivity.element_fields_device(op, u, 8)
+        ts = sensitivity.stress_sensitivity(op, u, lam)
+        design = torch.from_numpy(d.design_mask.astype(np.uint8)).cuda()
+        ls = levelset.combine_device([tj, ts], [2.0, 1.0])
+        stages = {
+            "element_state_TJ_pnorm": (lambda: sensitivity.element_fields_device(op, u, 8), 8.0 * (nd + 3 * ne)),
+            "adjoint_rhs": (lambda: sensitivity.adjoint_rhs_device(op, u, 8, sums), 8.0 * (2 * nd + ne)),
+            "stress_sensitivity": (lambda: sensitivity.stress_sensitivity(op, u, lam), 8.0 * (2 * nd + 2 * ne)),
+            "combine_2_fields": (lambda: levelset.combine_device([tj, ts], [2.0, 1.0]), 8.0 * 5 * ne),
+            "threshold_select": (lambda: levelset.extract_device(d, ls, 0.5, 1e-3, design), 16.0 * ne),
+        }
+        out = {}
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for name, (fn, nbytes) in stages.items():
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            a.record()
+            for _ in range(20):
+                fn()
+            e.record()
+            torch.cuda.synchronize()
+            us = 1e3 * a.elapsed_time(e) / 20
+            out[name] = {"us": us, "alg_bytes": nbytes, "gbs": nbytes / (us / 1e6) / 1e9,
+                         "frac_hbm": nbytes / (us / 1e6) / 1e9 / hbm}
+        out["note"] = ("timed through the public device API (includes its small allocations / host "
+                       "round trips: the select reads its 4-word state back)")
+        return out
+    except Exception as exc:  # pragma: no cover
+        return {"error": repr(exc)[:300]}
 
 
 def secondary_optimizer(torch, outer=3):

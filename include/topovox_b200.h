@@ -233,7 +233,9 @@ int tvb_pcg_solve(tvb_pcg_desc* desc, void* stream);
  * stopping test and iteration count, and its result is bitwise equal to
  * tvb_pcg_solve on it alone. Per-RHS outputs: h_iterations, h_residuals,
  * h_status (0 / NoConvergence / Singular ...). Returns the first failing
- * per-RHS status. d_ws >= tvb_pcg_batch_ws_bytes(). */
+ * per-RHS status, or the call's own error (bad arguments, workspace, CUDA),
+ * which is then also written to every h_status entry -- no failure path leaves
+ * a per-RHS status at 0. d_ws >= tvb_pcg_batch_ws_bytes(). */
 size_t tvb_pcg_batch_ws_bytes(int nx, int ny, int nz, int block, int nrhs);
 int tvb_pcg_solve_batch(tvb_pcg_desc* desc, int nrhs, const double* const* h_d_f, double* const* h_d_x,
                         int* h_iterations, double* h_residuals, int* h_status, void* stream);

@@ -308,9 +308,14 @@ class Deflation:
         return self._pinv @ y
 
 
-def solve_static(op: Operator, f, tol=1e-8, max_iters=None, deflation: Deflation | None = None):
+def solve_static(op: Operator, f, tol=1e-8, max_iters=None, deflation: Deflation | None = None, observer=None):
     """Deflated Jacobi PCG, step for step topovox/fea.py:218-299.
-    Returns (u, iterations, residual)."""
+    Returns (u, iterations, residual).
+
+    ``observer(it, x, res)`` (fixture generation only) is called after every
+    iteration's residual update; a true return value ends the loop there and
+    returns that iterate (fixed DOFs zeroed) as if it had converged. It does
+    not change any arithmetic of the loop."""
     if not 0.0 < tol <= 1e-2:
         raise ValueError("tolerance must lie in (0, 1e-2]")
     f = np.asarray(f, dtype=float)
@@ -350,6 +355,8 @@ def solve_static(op: Operator, f, tol=1e-8, max_iters=None, deflation: Deflation
         r -= alpha * q
         res = np.linalg.norm(r) / fnorm
         if res <= tol:
+            break
+        if observer is not None and observer(it, x, res):
             break
         z = inv_d * r
         rz_new = r @ z
@@ -684,9 +691,12 @@ def constraint_value(q, q0, alpha, sense):
 
 def run_optimizer(nx, ny, nz, cases, specs, E=1.0, nu=0.3, tol=1e-8, block=4, ersatz=1e-6, mu0=100.0, gamma0=10.0,
                   varsigma=0.25, eta=10.0, dv0=0.025, dv_min=0.005, growth=1.1, growth_after=3, inner_cap=10,
-                  ctol=0.01, ttol=0.001, feas=1e-6, max_outer=400, casting=None, rho=1.0):
+                  ctol=0.01, ttol=0.001, feas=1e-6, max_outer=400, casting=None, rho=1.0, trace=None):
     """Returns (occ, history list of dicts, reason). casting: (axis, parting
-    element layer) -> casting-projected extraction with all ties retained."""
+    element layer) -> casting-projected extraction with all ties retained.
+    trace(record) (fixture generation only) receives every extraction:
+    dict(k, it, occ = topology the fields were computed on, weights, target,
+    levelset, tau, new_occ)."""
     ne = nx * ny * nz
     design = np.ones(ne, dtype=bool)
     occ = np.ones(ne)
@@ -716,7 +726,10 @@ def run_optimizer(nx, ny, nz, cases, specs, E=1.0, nu=0.3, tol=1e-8, block=4, er
                             fallback=fb)
             if casting is not None:
                 ls = casting_project(ls, (nx, ny, nz), *casting)
-            new_occ, _, _ = extract(ls, design, target, ersatz, all_ties=casting is not None)
+            new_occ, tau, _ = extract(ls, design, target, ersatz, all_ties=casting is not None)
+            if trace is not None:
+                trace(dict(k=k, it=it, occ=cur_occ, weights=[w[i] for i in range(len(specs))], target=target,
+                           levelset=ls, tau=tau, new_occ=new_occ))
             if it > 1 and np.count_nonzero((new_occ == 1.0) != (cur_occ == 1.0)) < ttol * ne:
                 conv = True
                 break

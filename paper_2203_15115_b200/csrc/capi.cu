@@ -690,22 +690,37 @@ size_t tvb_pcg_batch_ws_bytes(int nx, int ny, int nz, int block, int nrhs) {
 
 int tvb_pcg_solve_batch(tvb_pcg_desc* d, int nrhs, const double* const* h_d_f, double* const* h_d_x,
                         int* h_iterations, double* h_residuals, int* h_status, void* stream) {
-  if (nrhs < 1 || nrhs > kPcgMaxRhs || !h_d_f || !h_d_x) return kStatusBadArg;
+  if (nrhs < 1 || nrhs > kPcgMaxRhs) return kStatusBadArg;
+  // every return path reports a per-RHS status: a failure of the whole call
+  // (arguments, problem, workspace, CUDA / graph) is never left as "ok"
+  auto fail_all = [&](int st) {
+    for (int c = 0; c < nrhs; ++c) {
+      if (h_iterations) h_iterations[c] = 0;
+      if (h_residuals) h_residuals[c] = 0.0;
+      if (h_status) h_status[c] = st;
+    }
+    return st;
+  };
+  if (!h_d_f || !h_d_x) return fail_all(kStatusBadArg);
   PcgProblem P{};
-  if (int st = pcg_problem(d, P)) return st;
+  if (int st = pcg_problem(d, P)) return fail_all(st);
   P.nrhs = nrhs;
   for (int c = 0; c < nrhs; ++c) {
-    if (!h_d_f[c] || !h_d_x[c]) return kStatusBadArg;
+    if (!h_d_f[c] || !h_d_x[c]) return fail_all(kStatusBadArg);
     P.fs[c] = h_d_f[c];
     P.xs[c] = h_d_x[c];
   }
-  PcgResult R[kPcgMaxRhs];
+  PcgResult R[kPcgMaxRhs] = {};
   int rs[kPcgMaxRhs];
+  for (int c = 0; c < nrhs; ++c) rs[c] = -1;  // not reached by the solver
   const int st = pcg_solve_multi(P, R, rs, (cudaStream_t)stream);
+  const bool call_failed = st != kStatusOk && st != kStatusNoConvergence;
   for (int c = 0; c < nrhs; ++c) {
+    int sc = rs[c];
+    if (sc == -1 || (call_failed && sc == kStatusOk)) sc = call_failed ? st : kStatusCuda;
     if (h_iterations) h_iterations[c] = R[c].iterations;
     if (h_residuals) h_residuals[c] = R[c].residual;
-    if (h_status) h_status[c] = rs[c];
+    if (h_status) h_status[c] = sc;
   }
   return st;
 }

@@ -33,12 +33,16 @@ class NoConvergence(TopovoxError):
     """Iterative solve stopped at its iteration cap.
 
     ``residual`` is the last relative residual, ``iterations`` the cap.
+    ``u`` (an addition to the reference's exception, None unless the solver
+    set it) is the iterate after the last iteration -- what a fixed-iteration
+    parity check compares.
     """
 
-    def __init__(self, message, residual=None, iterations=None):
+    def __init__(self, message, residual=None, iterations=None, u=None):
         super().__init__(message)
         self.residual = residual
         self.iterations = iterations
+        self.u = u
 
 
 class SingularSystem(TopovoxError):

@@ -459,7 +459,7 @@ def solve_static(op: StiffnessOperator, f, tol: float = 1.0e-8, max_iters: int |
     st = lib().tvb_pcg_solve(ctypes.byref(desc), stream_ptr())
     if st == STATUS_NO_CONVERGENCE:
         raise NoConvergence(f"CG did not reach {tol:g} in {max_iters} iterations (residual {desc.residual:.3e})",
-                            residual=desc.residual, iterations=max_iters)
+                            residual=desc.residual, iterations=max_iters, u=to_host_if(x, np_in))
     if st != 0:
         raise_for_status(st, "solve_static", _lib.last_error())
     return SolveResult(to_host_if(x, np_in), int(desc.iterations), float(desc.residual))
@@ -538,15 +538,24 @@ def solve_static_batch(op: StiffnessOperator, forces, tol: float = 1.0e-8, max_i
         its = (ctypes.c_int * m)()
         res = (ctypes.c_double * m)()
         sts = (ctypes.c_int * m)()
-        lib().tvb_pcg_solve_batch(ctypes.byref(desc), m, ctypes.cast(fptr, ctypes.c_void_p),
-                                  ctypes.cast(xptr, ctypes.c_void_p), ctypes.cast(its, ctypes.c_void_p),
-                                  ctypes.cast(res, ctypes.c_void_p), ctypes.cast(sts, ctypes.c_void_p), stream_ptr())
+        st = lib().tvb_pcg_solve_batch(ctypes.byref(desc), m, ctypes.cast(fptr, ctypes.c_void_p),
+                                       ctypes.cast(xptr, ctypes.c_void_p), ctypes.cast(its, ctypes.c_void_p),
+                                       ctypes.cast(res, ctypes.c_void_p), ctypes.cast(sts, ctypes.c_void_p),
+                                       stream_ptr())
+        # The call's own status is authoritative: a failure before or after the
+        # per-RHS loop (bad problem, workspace, CUDA / graph error) leaves the
+        # per-RHS array meaningless, so it is never read as success.
+        if st not in (0, STATUS_NO_CONVERGENCE):
+            raise_for_status(st, "solve_static_batch", _lib.last_error())
         for c in range(m):
             if sts[c] == STATUS_NO_CONVERGENCE:
                 raise NoConvergence(f"CG did not reach {tol:g} in {max_iters} iterations for right-hand side "
-                                    f"{g0 + c} (residual {res[c]:.3e})", residual=res[c], iterations=max_iters)
+                                    f"{g0 + c} (residual {res[c]:.3e})", residual=res[c], iterations=max_iters,
+                                    u=to_host_if(xs[c], np_flags[g0 + c]))
             if sts[c] != 0:
                 raise_for_status(sts[c], f"solve_static_batch (right-hand side {g0 + c})", _lib.last_error())
+        if st == STATUS_NO_CONVERGENCE:
+            raise NoConvergence(f"CG did not reach {tol:g} in {max_iters} iterations", iterations=max_iters)
         out.extend(SolveResult(to_host_if(xs[c], np_flags[g0 + c]), int(its[c]), float(res[c])) for c in range(m))
     return out
 
