@@ -259,6 +259,14 @@ def main():
     def step():
         op.apply_device(ud, yd)
 
+    # clock ramp (not a step): ~0.3 s of device writes so the SM clock is at
+    # its loaded value before the warm-up steps (a short run otherwise times
+    # its first steps at ramping clocks)
+    t_ramp = time.perf_counter()
+    while time.perf_counter() - t_ramp < 0.3:
+        for _ in range(8):
+            flush.fill_(1.0)
+        torch.cuda.synchronize()
     for i in range(max(3, args.warmup)):
         flush.fill_(float(i))
         step()

@@ -1,0 +1,63 @@
+"""How far does the REFERENCE's own DPCG iterate move under a benign rounding
+change? (build container only; evidence for the parity tolerances in
+tests/test_gpu_large_parity.py.)
+
+    python tests/golden/noise_floor.py [case]
+
+Runs the reference's loop (oracle restatement, bitwise equal to it) on the
+reference's operator and deflation space twice: coarse solve by sparse LU
+(the fixtures' choice) and by an explicit dense inverse of the same E (the
+reference's dense Cholesky is 1.6 s/iteration at n_c = 12,000). Prints the
+relative difference of the iterates at the fixture's recorded iteration
+counts, measured exactly like the GPU test (4096 sample DOFs)."""
+import os
+import sys
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+sys.dont_write_bytecode = True
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+sys.path.insert(0, os.path.dirname(HERE))
+
+import numpy as np  # noqa: E402
+from topovox import fea  # noqa: E402
+from topovox import mesh as refmesh  # noqa: E402
+from topovox.elements import Material  # noqa: E402
+
+import large_cases as LC  # noqa: E402
+from oracle import topovox_oracle as O  # noqa: E402
+from oracle.large import sparse_coarse_solver  # noqa: E402
+from make_large_fixtures import RefOp  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c3_bern"
+spec = LC.CASES[name]
+fx = np.load(os.path.join(HERE, "large_dpcg.npz"))
+d, fixed, f, occ = LC.problem(refmesh, spec)
+op = fea.StiffnessOperator(d, refmesh.Topology(d, occ), Material(E=1.0, nu=0.3), fixed)
+defl = fea.DeflationSpace(d, refmesh.Topology(d, occ), fixed, spec["block"])
+defl.prepare(op)
+E = np.asarray((defl.W.T @ defl.KW).todense())
+E = 0.5 * (E + E.T)
+idx = LC.sample_index(d.n_dofs)
+tags = sorted({k[len(name) + 1:].rsplit("_", 1)[0] for k in fx.files if k.startswith(name + "_") and k.endswith("_u")})
+its = sorted({int(fx[f"{name}_{t}_it"]) for t in tags})
+solvers = {"splu": sparse_coarse_solver(E), "dense_inverse": (lambda Ei: (lambda y: Ei @ y))(np.linalg.inv(E))}
+snaps = {}
+for sname, cs in solvers.items():
+    defl.coarse_solve = cs
+    defl.prepare = lambda *_a: None
+    got = {}
+
+    def obs(it, x, res):
+        if it in its:
+            got[it] = x[idx].copy()
+        return it >= its[-1]
+
+    O.solve_static(RefOp(op), f, tol=1e-14, max_iters=its[-1], deflation=defl, observer=obs)
+    snaps[sname] = got
+for it in its:
+    a, b = snaps["splu"][it], snaps["dense_inverse"][it]
+    ref = [fx[f"{name}_{t}_u"] for t in tags if int(fx[f"{name}_{t}_it"]) == it][0]
+    print(f"{name} x_{it}: splu vs dense inverse {np.linalg.norm(a - b) / np.linalg.norm(a):.2e}; "
+          f"splu vs fixture {np.linalg.norm(a - ref) / np.linalg.norm(ref):.2e}", flush=True)

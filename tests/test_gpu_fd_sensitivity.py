@@ -11,6 +11,8 @@ the field ranks elements by that loss (extraction keeps the largest values).
 The stress comparison uses the top-half stressed elements.
 """
 
+import math
+
 import numpy as np
 import pytest
 
@@ -44,7 +46,7 @@ def _removal_values(tv, d, fixed, fn):
     for e in elems:
         occ = base_occ.copy()
         occ[e] = tv.EPS_VOID
-        vals.append(fn(fea.StiffnessOperator(d, tv.Topology(d, occ), mat, fixed)))
+        vals.append(fn(fea.StiffnessOperator(d, tv.Topology(d, occ), mat, fixed))[0])
     return base, elems, np.array(vals)
 
 
@@ -59,11 +61,11 @@ def test_compliance_and_stress_fields_vs_element_removal():
 
     def analyse(op):
         u = fea.solve_static(op, f, tol=1e-12).u
-        return float(f @ u), sensitivity.pnorm_stress(op, u, P_NORM), op, u
+        return (float(f @ u), sensitivity.pnorm_stress(op, u, P_NORM)), op, u
 
-    (J0, s0, op, u), elems, rem = _removal_values(tv, d, fixed, analyse)
-    dJ = np.array([r[0] for r in rem]) - J0
-    ds = np.array([r[1] for r in rem]) - s0
+    ((J0, s0), op, u), elems, rem = _removal_values(tv, d, fixed, analyse)
+    dJ = rem[:, 0] - J0
+    ds = rem[:, 1] - s0
     tj = sensitivity.compliance_sensitivity(op, u)[elems]
     lam = sensitivity.stress_adjoint(op, u, P_NORM, tol=1e-12)
     ts = sensitivity.stress_sensitivity(op, u, lam)[elems]
@@ -89,7 +91,7 @@ def test_eigen_field_vs_element_removal():
         return float(r.values[0]), op, r.vectors[0]
 
     (w0, op, mode), elems, rem = _removal_values(tv, d, fixed, analyse)
-    loss = -(np.array([r[0] for r in rem]) - w0)
+    loss = -(rem - w0)
     t = eigen.eigen_sensitivity(op, mode, w0)
     t = (t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t))[elems]
     rho = _spearman(t, loss)
@@ -109,11 +111,14 @@ def test_buckling_field_vs_element_removal():
     def analyse(op):
         u = fea.solve_static(op, f, tol=1e-12).u
         geo = eigen.geometric_stiffness(u, op)
-        r = eigen.solve_buckling(op, geo, k=1, tol=1e-10)
+        # no search cap: the cap (10 % strain, a builder heuristic) reacts to the
+        # floating EPS_VOID nodes a removal next to the hole or a corner creates
+        r = eigen.solve_buckling(op, geo, k=1, tol=1e-10, lambda_cap=math.inf)
+        assert not r.no_positive_factor
         return float(r.values[0]), op, geo, r.vectors[0]
 
     (l0, op, geo, mode), elems, rem = _removal_values(tv, d, fixed, analyse)
-    loss = -(np.array([r[0] for r in rem]) - l0)
+    loss = -(rem - l0)
     t = eigen.buckling_sensitivity(op, geo, mode, l0)
     t = (t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t))[elems]
     rho = _spearman(t, loss)
