@@ -193,6 +193,40 @@ typedef struct tvb_coarse_nd {
 } tvb_coarse_nd;
 int tvb_coarse_nd_solve(const tvb_coarse_nd* nd, const double* d_y, double* d_x, void* stream);
 
+/* ---- K6: numeric factorisation of the coarse operator (replaces
+ * scipy.linalg.cho_factor(E), topovox/fea.py:197-205) ----------------------
+ * Fronts of the nested-dissection tree (coarse.py) -- or one front holding
+ * all of E for small coarse spaces -- reduced on the device by the block
+ * sweep operator (csrc/dense.cu). d_fronts: int64[n][12] records
+ * (a_off, nf, s, s_pad, u, blk_off, nchild, child_off, scr_off, ntf, 0, 0);
+ * d_children: int64 pairs (child front, gmap offset); d_gmap: int32 parent
+ * front position -> child update index or -1; d_blocks: natural block ids of
+ * each front (separator, then update set); d_Es: block stencil f64[nb][27][36].
+ * d_err is set nonzero when a pivot is not positive (E not SPD). */
+typedef struct tvb_front_set {
+  const void* d_fronts;
+  double* d_pool;
+  double* d_scratch;
+  const int* d_blocks;
+  const long long* d_children;
+  const int* d_gmap;
+  const double* d_Es;
+  int mx, my, mz;
+  int* d_err;
+} tvb_front_set;
+
+/* assemble and sweep every front of one tree height: d_level_fronts (n_fronts
+ * indices), d_tiles (n_tiles (front, I, J) lower 64x64 tiles), d_cols
+ * (n_cols (front, K) tile columns), max_steps = max separator tiles */
+int tvb_front_level(const tvb_front_set* fs, int n_fronts, const int* d_level_fronts, int n_tiles,
+                    const int* d_tiles, int n_cols, const int* d_cols, int max_steps, void* stream);
+/* G (u x s) and [Z | -G^T] (s x (s + u)) of a swept front, row-major */
+int tvb_front_pack(const tvb_front_set* fs, int front, double* d_G, double* d_B, long long s, long long u,
+                   void* stream);
+/* Z = F^-1 of a fully swept front of order n: tiles > 0 -> lower 64x64 tiles
+ * (tile I (I + 1) / 2 + J, row-major, zero padded), tiles == 0 -> dense rows */
+int tvb_front_pack_top(const tvb_front_set* fs, int front, long long n, int tiles, double* d_out, void* stream);
+
 /* a8: (deflated) Jacobi PCG -- replaces solve_static (fea.py:218-299).
  * Synchronous: returns after convergence / the iteration cap. */
 typedef struct tvb_pcg_desc {
@@ -217,6 +251,11 @@ typedef struct tvb_pcg_desc {
   const double* d_coarse;   /* coarse_kind 0: dense inverse f64[nc*nc] */
   int coarse_kind;          /* 0 = dense inverse, 1 = nested dissection (coarse_nd) */
   const tvb_coarse_nd* coarse_nd;
+  /* deflated search direction (equal in exact arithmetic):
+   *   0 = the reference's recurrence p = z + beta p - W E^-1 (AW)^T z (fea.py:289)
+   *   1 = stabilised:               p = z + beta p - W E^-1 W^T (A z + beta A p_old),
+   *       which re-imposes W^T A p = 0 every iteration (robust at tol ~1e-12) */
+  int projection;
   /* outputs */
   int iterations;
   double residual;

@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtopovox_b200.so")
-SOURCES = ["capi.cu", "matvec.cu", "vec.cu", "deflation.cu", "solver.cu", "fields.cu", "coarse.cu", "eigen.cu"]
+SOURCES = ["capi.cu", "matvec.cu", "vec.cu", "deflation.cu", "solver.cu", "fields.cu", "coarse.cu", "eigen.cu", "dense.cu"]
 NVCC_FLAGS = [
     "-std=c++17", "-O3", "-lineinfo",
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -41,6 +41,13 @@ class CoarseND(ctypes.Structure):
     ]
 
 
+class FrontSet(ctypes.Structure):
+    _fields_ = [
+        ("d_fronts", P), ("d_pool", P), ("d_scratch", P), ("d_blocks", P), ("d_children", P), ("d_gmap", P),
+        ("d_Es", P), ("mx", c_int), ("my", c_int), ("mz", c_int), ("d_err", P),
+    ]
+
+
 class PcgDesc(ctypes.Structure):
     _fields_ = [
         ("nx", c_int), ("ny", c_int), ("nz", c_int),
@@ -51,6 +58,7 @@ class PcgDesc(ctypes.Structure):
         ("tol", c_double), ("max_iters", c_int), ("check_every", c_int),
         ("block", c_int), ("d_cen", P), ("d_S", P), ("d_keep", P),
         ("d_coarse", P), ("coarse_kind", c_int), ("coarse_nd", ctypes.POINTER(CoarseND)),
+        ("projection", c_int),
         ("iterations", c_int), ("residual", c_double), ("fnorm", c_double),
     ]
 
@@ -79,6 +87,9 @@ _SIGS = {
     "tvb_coarse_assemble": (c_int, [c_int, c_int, c_int, c_int, c_double, P, P, P, P, P, P, P, P, c_size_t, P]),
     "tvb_coarse_dense": (c_int, [c_int, c_int, c_int, c_int, P, P, P]),
     "tvb_coarse_nd_solve": (c_int, [ctypes.POINTER(CoarseND), P, P, P]),
+    "tvb_front_level": (c_int, [ctypes.POINTER(FrontSet), c_int, P, c_int, P, c_int, P, c_int, P]),
+    "tvb_front_pack": (c_int, [ctypes.POINTER(FrontSet), c_int, P, P, c_ll, c_ll, P]),
+    "tvb_front_pack_top": (c_int, [ctypes.POINTER(FrontSet), c_int, c_ll, c_int, P, P]),
     "tvb_pcg_ws_bytes": (c_size_t, [c_int, c_int, c_int, c_int]),
     "tvb_pcg_solve": (c_int, [ctypes.POINTER(PcgDesc), P]),
     "tvb_pcg_batch_ws_bytes": (c_size_t, [c_int, c_int, c_int, c_int, c_int]),

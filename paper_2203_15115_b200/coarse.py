@@ -12,8 +12,9 @@ so it is factored here by geometric nested dissection:
   ancestor-separator blocks adjacent to the node's box). Coarse DOFs are
   renumbered in ND order (separators by increasing tree height), so every
   separator is a contiguous DOF range and the top levels form the tail.
-* numeric (device, once per operator): multifrontal block LDL^T for the
-  "bottom" nodes (height < H0): per node, in order of height,
+* numeric (device, once per operator): multifrontal elimination of the
+  "bottom" nodes (height < H0): per node, in order of height (block sweep of
+  the separator, csrc/dense.cu),
       Z = F_SS^-1,  G = F_US Z,  update = F_UU - G F_SU  (to the parent front);
   the "top" nodes (height >= H0, at most TOP_MAX DOFs in total) are not
   factored node by node: their Schur complement S_T (original entries among
@@ -29,8 +30,9 @@ so it is factored here by geometric nested dissection:
   The exact coarse solve keeps the DPCG iterates identical (up to rounding) to
   the reference's dense Cholesky.
 
-The dense per-front linear algebra of the factorisation uses torch on the
-device (cuSOLVER/cuBLAS); it runs once per topology, not per iteration.
+The numeric factorisation (once per topology) runs in hand-written kernels
+too (csrc/dense.cu, ``front_plan``): every front of a tree height is
+assembled and swept in one launch sequence; no cuSOLVER / cuBLAS.
 """
 
 from __future__ import annotations
@@ -151,13 +153,116 @@ def _dofs(first_block_pos: np.ndarray) -> np.ndarray:
     return (6 * first_block_pos[:, None] + np.arange(6)[None, :]).ravel()
 
 
+FT = 64  # tile order of the device front factorisation (csrc/dense.cuh kFT)
+
+
+def _roundup(x: int, m: int = FT) -> int:
+    return -(-int(x) // m) * m
+
+
+def front_plan(torch, dev, specs):
+    """Device records of the front factorisation (csrc/dense.cu).
+
+    ``specs``: per front (natural block ids -- separator then update set --,
+    separator DOFs s, update DOFs u, [(child front index, child update block
+    ids in the child's order)], level). A child's update block list maps into
+    the parent front through the parent's block positions. Returns the
+    records, pool / scratch sizes and per-level launch lists."""
+    n = len(specs)
+    rec = np.zeros((n, 12), dtype=np.int64)
+    blocks, children, gmap = [], [], []
+    blk_off = gm_off = child_cnt = 0
+    a_off = 0
+    levels = {}
+    for f, (blk, s, u, kids, level) in enumerate(specs):
+        s_pad, nf = _roundup(s), _roundup(s) + _roundup(u)
+        pos = {int(b): i for i, b in enumerate(blk)}
+        rec[f, :10] = (a_off, nf, s, s_pad, u, blk_off, len(kids), child_cnt, 0, nf // FT)
+        for cf, cupd in kids:
+            g = -np.ones(s + u, dtype=np.int32)
+            ppos = np.array([pos[int(b)] for b in cupd], dtype=np.int64)
+            g[_dofs(ppos)] = np.arange(6 * cupd.size, dtype=np.int32)
+            children.append((cf, gm_off))
+            gmap.append(g)
+            gm_off += g.size
+            child_cnt += 1
+        blocks.append(np.asarray(blk, dtype=np.int32))
+        blk_off += len(blk)
+        a_off += nf * nf
+        levels.setdefault(level, []).append(f)
+    out_levels, scratch = [], 0
+    for level in sorted(levels):
+        fr = levels[level]
+        off = 0
+        tiles, cols = [], []
+        for f in fr:
+            ntf = int(rec[f, 9])
+            rec[f, 8] = off
+            off += (1 + 2 * ntf) * FT * FT
+            I, J = np.tril_indices(ntf)
+            tiles.append(np.stack([np.full(I.size, f), I, J], axis=1))
+            cols.append(np.stack([np.full(ntf, f), np.arange(ntf)], axis=1))
+        scratch = max(scratch, off)
+        tiles = np.concatenate(tiles).astype(np.int32)
+        cols = np.concatenate(cols).astype(np.int32)
+        out_levels.append({"fronts": torch.from_numpy(np.array(fr, dtype=np.int32)).to(dev), "n": len(fr),
+                           "tiles": torch.from_numpy(np.ascontiguousarray(tiles)).to(dev), "nt": tiles.shape[0],
+                           "cols": torch.from_numpy(np.ascontiguousarray(cols)).to(dev), "nc": cols.shape[0],
+                           "steps": int(max(rec[f, 3] for f in fr)) // FT})
+    return {"rec": torch.from_numpy(rec).to(dev),
+            "blocks": torch.from_numpy(np.concatenate(blocks)).to(dev),
+            "children": torch.from_numpy(np.array(children or [(0, 0)], dtype=np.int64)).to(dev),
+            "gmap": torch.from_numpy(np.concatenate(gmap) if gmap else np.zeros(1, np.int32)).to(dev),
+            "levels": out_levels, "pool": max(a_off, 1), "scratch": max(scratch, 1)}
+
+
+def front_set(fp, pool, scratch, Es, grid, err):
+    """tvb_front_set of a front plan; keeps its tensors alive on the struct."""
+    from ._lib import FrontSet
+
+    fs = FrontSet()
+    fs.d_fronts, fs.d_pool, fs.d_scratch = ptr(fp["rec"]), ptr(pool), ptr(scratch)
+    fs.d_blocks, fs.d_children, fs.d_gmap = ptr(fp["blocks"]), ptr(fp["children"]), ptr(fp["gmap"])
+    fs.d_Es = ptr(Es)
+    fs.mx, fs.my, fs.mz = grid
+    fs.d_err = ptr(err)
+    fs._keep = (fp, pool, scratch, Es, err)
+    return fs
+
+
+def run_front_levels(fs, levels):
+    for L in levels:
+        check(lib().tvb_front_level(ctypes.byref(fs), L["n"], ptr(L["fronts"]), L["nt"], ptr(L["tiles"]), L["nc"],
+                                    ptr(L["cols"]), L["steps"], stream_ptr()), "front factorisation")
+
+
+def dense_inverse(grid, Es):
+    """E^-1 (natural block order, dense rows) of a small coarse space: E as one
+    front with no update set, swept on the device. Raises LinAlgError when E
+    is not SPD."""
+    import torch
+
+    nb = grid[0] * grid[1] * grid[2]
+    fp = front_plan(torch, Es.device, [(np.arange(nb), 6 * nb, 0, [], 0)])
+    pool = torch.empty(fp["pool"], dtype=torch.float64, device=Es.device)
+    scratch = torch.empty(fp["scratch"], dtype=torch.float64, device=Es.device)
+    err = torch.zeros(1, dtype=torch.int32, device=Es.device)
+    fs = front_set(fp, pool, scratch, Es, grid, err)
+    run_front_levels(fs, fp["levels"])
+    out = torch.empty((6 * nb, 6 * nb), dtype=torch.float64, device=Es.device)
+    check(lib().tvb_front_pack_top(ctypes.byref(fs), 0, 6 * nb, 0, ptr(out), stream_ptr()), "front pack")
+    if int(err.item()) != 0:
+        raise np.linalg.LinAlgError("coarse matrix not SPD")
+    return out
+
+
 class NDCoarseSolver:
     """Factor E (block stencil ``Es`` on the device, natural block order) and
     hold the device data of the per-iteration solve (``tvb_coarse_nd_solve``).
     Solve vectors are in ND order: natural block B sits at ND block ``perm[B]``."""
 
     def __init__(self, grid: tuple[int, int, int], Es, leaf_max: int | None = None, top_max: int | None = None,
-                 make_desc: bool = True):
+                 make_desc: bool = True, numeric: bool = True):
         import torch
 
         mx, my, mz = grid
@@ -201,54 +306,23 @@ class NDCoarseSolver:
         self.flow = FLOW != "0" if FLOW is not None else 6 * nb >= FLOW_MIN_DOFS
         #: packed symmetric top tiles (per-level schedule; the dataflow kernel reads dense rows)
         self.top_tiles = (self.n_top + TOP_TILE - 1) // TOP_TILE if (self.n_top and not self.flow and PACK_TOP) else 0
-        self._factor(torch, Es, nodes, bottom, top, bidx, perm)
+        self.bottom_nodes, self.top_nodes = bottom, top
+        # numeric=False (CPU tests of the symbolic layout and the solve
+        # schedule only): the factor arrays are allocated but left for the
+        # caller to fill; nothing on the product path passes it
+        self._factor(torch, Es, nodes, bottom, top, bidx, perm, numeric)
         self._make = make_desc
         self.desc = self._make_desc() if make_desc else None
 
-    # ------------------------------------------------------------------
-    def _stencil_entries(self, rows_blocks, pos):
-        """(row pos, col pos, source block, neighbour slot) of the original E
-        entries with the row in ``rows_blocks`` and the column at pos >= 0."""
-        mx, my, mz = self.grid
-        sb = rows_blocks
-        x, y, z = sb % mx, (sb // mx) % my, sb // (mx * my)
-        out = [[], [], [], []]
-        for d in range(27):
-            cx, cy, cz = x + d % 3 - 1, y + (d // 3) % 3 - 1, z + d // 9 - 1
-            ok = (cx >= 0) & (cx < mx) & (cy >= 0) & (cy < my) & (cz >= 0) & (cz < mz)
-            cb = np.where(ok, cx + mx * (cy + my * cz), 0)
-            pc = np.where(ok, pos[cb], -1)
-            keep = ok & (pc >= 0)
-            out[0].append(np.arange(sb.size)[keep])
-            out[1].append(pc[keep])
-            out[2].append(sb[keep])
-            out[3].append(np.full(int(keep.sum()), d))
-        return [np.concatenate(o) for o in out]
-
-    def _flat_scatter(self, rows, cols, srcB, srcD, nf, mirror_from):
-        """Flat indices for F.view(-1)[fidx] = Es.view(-1)[eidx]: the 6x6 blocks
-        E[srcB, srcD] at block position (rows, cols) of an nf x nf front, plus
-        their transposes at (cols, rows) for cols >= mirror_from (block units)."""
-        i = np.arange(6)[None, :, None]
-        j = np.arange(6)[None, None, :]
-        r6, c6 = 6 * rows[:, None, None], 6 * cols[:, None, None]
-        e = ((srcB[:, None, None] * 27 + srcD[:, None, None]) * 6 + i) * 6 + j
-        f = (r6 + i) * nf + (c6 + j)
-        fl, el = [f.ravel()], [e.ravel()]
-        if mirror_from is not None:
-            m = cols >= mirror_from
-            if m.any():
-                fl.append(((c6[m] + j) * nf + (r6[m] + i)).ravel())
-                el.append(e[m].ravel())
-        return np.concatenate(fl), np.concatenate(el)
-
     def _plan(self, torch, dev, nodes, bottom, top, perm):
-        """Index plan of the numeric factorisation (depends on the block grid
-        only, so it is cached across topologies): per bottom node the flat
-        scatter of its original E entries into the front, the extend-add
-        positions of its children's updates, and the same for the dense top."""
+        """Index plan (depends on the block grid only, so it is cached across
+        topologies): the solve's per-node layout (separator / update sizes,
+        update-DOF maps, gathered front positions) and the device front
+        records of the numeric factorisation (``front_plan``)."""
         nb = self.nb
-        P = {"nodes": [], "top": None}
+        P = {}
+        bidx_of = {ni: k for k, ni in enumerate(bottom)}
+        tblocks = np.concatenate([nodes[i].sep for i in top]).astype(np.int64) if top else np.zeros(0, np.int64)
         ud_off = {}
         ud_cursor = 0
         blk_cursor = 0
@@ -260,18 +334,12 @@ class NDCoarseSolver:
             nf = 6 * front.size
             pos = -np.ones(nb, dtype=np.int64)
             pos[front] = np.arange(front.size)
-            rows, cols, srcB, srcD = self._stencil_entries(n.sep, pos)
-            fidx, eidx = self._flat_scatter(rows, cols, srcB, srcD, nf, ns)
             gm = -np.ones((nf, 2), dtype=np.int64)
             assert len(n.children) <= 2
-            adds = []
             for k, c in enumerate(n.children):
                 m = _dofs(pos[nodes[c].upd])
-                adds.append((c, torch.from_numpy((m[:, None] * nf + m[None, :]).ravel()).to(dev)))
                 gm[m, k] = ud_off[c] + np.arange(m.size)
             gmaps.append(gm.astype(np.int32).ravel())
-            P["nodes"].append((ni, nf, 6 * ns, nu, torch.from_numpy(fidx).to(dev), torch.from_numpy(eidx).to(dev),
-                               adds))
             s_list.append(6 * ns)
             u_list.append(6 * nu)
             sd_list.append(6 * blk_cursor)
@@ -281,24 +349,31 @@ class NDCoarseSolver:
             udof_list.append(_dofs(perm[n.upd]).astype(np.int32))
         t_pos, t_idx = [], []
         if self.n_top:
-            tblocks = np.concatenate([nodes[i].sep for i in top]).astype(np.int64)
             tpos = -np.ones(nb, dtype=np.int64)
             tpos[tblocks] = perm[tblocks] - (nb - tblocks.size)
-            rows, cols, srcB, srcD = self._stencil_entries(tblocks, tpos)
-            fidx, eidx = self._flat_scatter(tpos[srcB], cols, srcB, srcD, self.n_top, None)
-            adds = []
             for ni in bottom:
                 if nodes[ni].parent >= 0 and nodes[nodes[ni].parent].height >= self.H0:
                     m = _dofs(tpos[nodes[ni].upd])
-                    adds.append((ni, torch.from_numpy((m[:, None] * self.n_top + m[None, :]).ravel()).to(dev)))
                     t_pos.append(m)
                     t_idx.append(ud_off[ni] + np.arange(m.size))
-            P["top"] = (torch.from_numpy(fidx).to(dev), torch.from_numpy(eidx).to(dev), adds)
         P["pack"] = (np.array(s_list, np.int64), np.array(u_list, np.int64), np.array(sd_list, np.int64),
                      udof_list, gmaps, t_pos, t_idx, ud_cursor, [nodes[i].height for i in bottom])
+        specs = []
+        for ni in bottom:
+            n = nodes[ni]
+            specs.append((np.concatenate([n.sep, n.upd]), 6 * n.sep.size, 6 * n.upd.size,
+                          [(bidx_of[c], nodes[c].upd) for c in n.children], n.height))
+        if self.n_top:
+            tchild = [(bidx_of[ni], nodes[ni].upd) for ni in bottom
+                      if nodes[ni].parent >= 0 and nodes[nodes[ni].parent].height >= self.H0]
+            specs.append((tblocks, self.n_top, 0, tchild, self.H0))
+        P["front"] = front_plan(torch, dev, specs)
         return P
 
-    def _factor(self, torch, Es, nodes, bottom, top, bidx, perm):
+    def _factor(self, torch, Es, nodes, bottom, top, bidx, perm, numeric=True):
+        """Numeric factorisation on the device (csrc/dense.cu, one launch
+        sequence per tree height: assemble the fronts, sweep their separators),
+        then the per-iteration layouts written by the pack kernels."""
         dev = Es.device
         key = (self.grid, self.leaf_max, self.top_max, str(dev))
         plan = _PLAN_CACHE.get(key)
@@ -306,41 +381,19 @@ class NDCoarseSolver:
             plan = self._plan(torch, dev, nodes, bottom, top, perm)
             _PLAN_CACHE.clear()  # keep one plan (one block grid per optimisation run)
             _PLAN_CACHE[key] = plan
-        Ef = Es.reshape(-1)
-        upd = {}
-        G_list, B_list, infos = [], [], []
-        for ni, nf, S, nu, fidx, eidx, adds in plan["nodes"]:
-            F = torch.zeros(nf * nf, dtype=torch.float64, device=dev)
-            F[fidx] = Ef[eidx]
-            for c, cidx in adds:
-                F[cidx] += upd.pop(c).reshape(-1)
-            F = F.view(nf, nf)
-            L, info = torch.linalg.cholesky_ex(0.5 * (F[:S, :S] + F[:S, :S].T))
-            infos.append(info)
-            Z = torch.cholesky_inverse(L)
-            G = F[S:, :S] @ Z
-            if nu:
-                upd[ni] = F[S:, S:] - G @ F[:S, S:]
-            G_list.append(G.contiguous())
-            B_list.append(torch.cat([Z, -G.T], dim=1).contiguous())   # x_S = [Z | -G^T] [f_S ; x_U]
-            del F
-        # ---- dense top: S_T = E_TT + updates of bottom nodes with a top parent
-        self.Ztop = None
-        if self.n_top:
-            fidx, eidx, adds = plan["top"]
-            ST = torch.zeros(self.n_top * self.n_top, dtype=torch.float64, device=dev)
-            ST[fidx] = Ef[eidx]
-            for ni, cidx in adds:
-                ST[cidx] += upd.pop(ni).reshape(-1)
-            ST = ST.view(self.n_top, self.n_top)
-            L, info = torch.linalg.cholesky_ex(0.5 * (ST + ST.T))
-            infos.append(info)
-            self.Ztop = torch.cholesky_inverse(L).contiguous()
-            del ST, L
-        assert not upd, "unconsumed update matrices"
-        if infos and bool(torch.stack(infos).ne(0).any()):  # one host sync for all fronts
+        fp = plan["front"]
+        if not numeric:
+            self._pack(torch, dev, None, len(bottom), *plan["pack"])
+            return
+        pool = torch.empty(fp["pool"], dtype=torch.float64, device=dev)
+        scratch = torch.empty(fp["scratch"], dtype=torch.float64, device=dev)
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        fs = front_set(fp, pool, scratch, Es, self.grid, err)
+        run_front_levels(fs, fp["levels"])
+        self._pack(torch, dev, fs, len(bottom), *plan["pack"])
+        if int(err.item()) != 0:  # one host sync for all fronts
             raise np.linalg.LinAlgError("coarse front not SPD")
-        self._pack(torch, dev, G_list, B_list, *plan["pack"])
+        del pool, scratch
 
     @staticmethod
     def _wpr(rowlen: int, rows: int) -> int:
@@ -375,8 +428,7 @@ class NDCoarseSolver:
             rpw *= 2
         return 1 if rpw == 1 else 1 | (rpw << 4)
 
-    def _pack(self, torch, dev, G_list, B_list, s, u, sd, udof_list, gmaps, t_pos, t_idx, n_cu, heights):
-        nbot = len(G_list)
+    def _pack(self, torch, dev, fs, nbot, s, u, sd, udof_list, gmaps, t_pos, t_idx, n_cu, heights):
         self.n_bottom = nbot
         self.s, self.u = s, u
         g_off = np.zeros(nbot + 1, dtype=np.int64)
@@ -392,25 +444,18 @@ class NDCoarseSolver:
         self.G = self.factor[:ng + 1]
         self.B = self.factor[ng + 1:ng + nbb + 2]
         self.ZT = self.factor[ng + nbb + 2:]
-        if ng:
-            self.G[:ng] = torch.cat([g.reshape(-1) for g in G_list])
-        if nbb:
-            self.B[:nbb] = torch.cat([b.reshape(-1) for b in B_list])
-        if ntop2 and nt:
-            # lower 64x64 tiles of the (symmetric) inverse, tile I*(I+1)/2 + J, row-major, zero-padded
-            n = self.n_top
-            Zp = torch.zeros(nt * TOP_TILE, nt * TOP_TILE, dtype=torch.float64, device=dev)
-            Zp[:n, :n] = self.Ztop
-            tiles = Zp.view(nt, TOP_TILE, nt, TOP_TILE).permute(0, 2, 1, 3)
-            Ii, Jj = np.tril_indices(nt)
-            self.ZT[:ntop2] = tiles[torch.from_numpy(Ii).to(dev), torch.from_numpy(Jj).to(dev)].reshape(-1)
-            del Zp, tiles
+        self.g_off, self.b_off = g_off, b_off
+        base = self.factor.data_ptr()
+        for k in range(nbot if fs is not None else 0):  # G (u x s) and B = [Z | -G^T] (s x (s + u)) of every bottom front
+            check(lib().tvb_front_pack(ctypes.byref(fs), k, base + 8 * int(g_off[k]), base + 8 * (ng + 1 + int(b_off[k])),
+                                       int(s[k]), int(u[k]), stream_ptr()), "front pack")
+        if ntop2 and fs is not None:  # the top inverse: lower 64x64 tiles or dense rows
+            check(lib().tvb_front_pack_top(ctypes.byref(fs), nbot, self.n_top, nt, base + 8 * (ng + nbb + 2),
+                                           stream_ptr()), "front pack top")
+        if nt:
             self.tpart = torch.zeros(MAX_COLS, nt * nt * TOP_TILE, dtype=torch.float64, device=dev)
-        elif ntop2:
-            self.ZT[:ntop2] = self.Ztop.reshape(-1)
-        if not nt:
+        else:
             self.tpart = None
-        self.Ztop = None
         ud_off = np.zeros(nbot + 1, dtype=np.int64)
         if nbot:
             ud_off[1:] = np.cumsum(u)

@@ -8,6 +8,7 @@
 
 #include "../../include/topovox_b200.h"
 #include "coarse.cuh"
+#include "dense.cuh"
 #include "deflation.cuh"
 #include "eigen.cuh"
 #include "fields.cuh"
@@ -661,6 +662,8 @@ static int pcg_problem(const tvb_pcg_desc* d, PcgProblem& P) {
   P.keep = d->d_keep;
   P.coarse = d->d_coarse;
   P.coarse_kind = d->coarse_kind;
+  if (d->projection != 0 && d->projection != 1) return kStatusBadArg;
+  P.stabilized = d->projection == 1;
   if (P.coarse_kind == 1) {
     if (!d->coarse_nd) return kStatusBadArg;
     P.nd = coarse_nd_dev(d->coarse_nd);
@@ -723,6 +726,49 @@ int tvb_pcg_solve_batch(tvb_pcg_desc* d, int nrhs, const double* const* h_d_f, d
     if (h_status) h_status[c] = sc;
   }
   return st;
+}
+
+static_assert(sizeof(FrontRec) == 12 * sizeof(long long), "front record layout");
+
+static bool front_set(const tvb_front_set* fs, FrontFactor& F) {
+  if (!fs || !fs->d_fronts || !fs->d_pool || !fs->d_blocks || !fs->d_Es || !fs->d_err || fs->mx < 1 || fs->my < 1 ||
+      fs->mz < 1)
+    return false;
+  F.fronts = (const FrontRec*)fs->d_fronts;
+  F.pool = fs->d_pool;
+  F.scratch = fs->d_scratch;
+  F.blocks = fs->d_blocks;
+  F.children = fs->d_children;
+  F.gmap = fs->d_gmap;
+  F.Es = fs->d_Es;
+  F.mx = fs->mx;
+  F.my = fs->my;
+  F.mz = fs->mz;
+  F.d_err = fs->d_err;
+  return true;
+}
+
+int tvb_front_level(const tvb_front_set* fs, int n_fronts, const int* d_level_fronts, int n_tiles,
+                    const int* d_tiles, int n_cols, const int* d_cols, int max_steps, void* stream) {
+  FrontFactor F;
+  if (!front_set(fs, F) || n_fronts < 1 || !d_level_fronts || n_tiles < 1 || !d_tiles || n_cols < 1 || !d_cols ||
+      max_steps < 0 || !fs->d_scratch)
+    return kStatusBadArg;
+  FrontLevel L{n_fronts, d_level_fronts, n_tiles, d_tiles, n_cols, d_cols, max_steps};
+  return check(launch_front_level(F, L, (cudaStream_t)stream));
+}
+
+int tvb_front_pack(const tvb_front_set* fs, int front, double* d_G, double* d_B, long long s, long long u,
+                   void* stream) {
+  FrontFactor F;
+  if (!front_set(fs, F) || front < 0 || !d_B || (u > 0 && !d_G) || s < 1 || u < 0) return kStatusBadArg;
+  return check(launch_front_pack(F, front, d_G, d_B, s, u, (cudaStream_t)stream));
+}
+
+int tvb_front_pack_top(const tvb_front_set* fs, int front, long long n, int tiles, double* d_out, void* stream) {
+  FrontFactor F;
+  if (!front_set(fs, F) || front < 0 || n < 1 || tiles < 0 || !d_out) return kStatusBadArg;
+  return check(launch_front_pack_top(F, front, n, tiles, d_out, (cudaStream_t)stream));
 }
 
 int tvb_coarse_nd_solve(const tvb_coarse_nd* nd, const double* d_y, double* d_x, void* stream) {

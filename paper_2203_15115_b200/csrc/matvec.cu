@@ -120,13 +120,15 @@ constexpr int kRing = kAhead + 1;
 //   apply the element operator in mode space, z-accumulate the node sums of
 //   plane k in mode space (carry), and exchange the 3 non-owned face nodes of
 //   plane k through shared memory; the owner thread finishes the node.
-template <int NT, int MINB, bool DOT, bool MASKOUT>
+// WX, WY > 0: the tile shape as compile-time constants (every index and
+// shared-memory offset of the hot loop becomes an immediate); 0: runtime shape.
+template <int NT, int MINB, bool DOT, bool MASKOUT, int WX = 0, int WY = 0>
 __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
   pdl_entry();
   extern __shared__ double smem[];
   if (P.stop != nullptr && *P.stop) return;
   const Grid& G = P.g;
-  const int wx = P.wx, wy = P.wy;
+  const int wx = WX > 0 ? WX : P.wx, wy = WY > 0 ? WY : P.wy;
   const int PW = wx + 1, PH = wy + 1;
   const int S = plane_row_stride(wx);
   const int PS = PH * S;   // doubles per staged node plane
@@ -424,21 +426,39 @@ MatvecPlan plan_matvec(const Grid& g, int num_sms) {
   return best;
 }
 
-template <int NT, int MINB>
+template <int NT, int MINB, int WX = 0, int WY = 0>
 static void set_smem_attr(size_t bytes) {
-  cudaFuncSetAttribute(k_matvec<NT, MINB, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  cudaFuncSetAttribute(k_matvec<NT, MINB, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  cudaFuncSetAttribute(k_matvec<NT, MINB, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  cudaFuncSetAttribute(k_matvec<NT, MINB, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  cudaFuncSetAttribute(k_matvec<NT, MINB, false, false, WX, WY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  cudaFuncSetAttribute(k_matvec<NT, MINB, false, true, WX, WY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  cudaFuncSetAttribute(k_matvec<NT, MINB, true, false, WX, WY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  cudaFuncSetAttribute(k_matvec<NT, MINB, true, true, WX, WY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-template <int NT, int MINB>
+template <int NT, int MINB, int WX = 0, int WY = 0>
 static void launch_nt(dim3 grid, size_t smem, cudaStream_t s, const MatvecParams& P, const Modal& M) {
   const bool dot = P.dot_partial != nullptr, mo = P.mask_out && P.fixed != nullptr;
-  if (dot && mo) launch_k(k_matvec<NT, MINB, true, true>, grid, NT, smem, s, P, M);
-  else if (dot) launch_k(k_matvec<NT, MINB, true, false>, grid, NT, smem, s, P, M);
-  else if (mo) launch_k(k_matvec<NT, MINB, false, true>, grid, NT, smem, s, P, M);
-  else launch_k(k_matvec<NT, MINB, false, false>, grid, NT, smem, s, P, M);
+  if (dot && mo) launch_k(k_matvec<NT, MINB, true, true, WX, WY>, grid, NT, smem, s, P, M);
+  else if (dot) launch_k(k_matvec<NT, MINB, true, false, WX, WY>, grid, NT, smem, s, P, M);
+  else if (mo) launch_k(k_matvec<NT, MINB, false, true, WX, WY>, grid, NT, smem, s, P, M);
+  else launch_k(k_matvec<NT, MINB, false, false, WX, WY>, grid, NT, smem, s, P, M);
+}
+
+// tile shapes compiled with constant geometry: the planner's choices for the
+// BASELINE grids (C2 23x11, C4 25x10, C5 28x9, C1 / C3 42x6)
+static bool launch_fixed_shape(const MatvecPlan& pl, dim3 grid, cudaStream_t s, const MatvecParams& P, const Modal& M) {
+  static const bool off = getenv("TVB_MV_GENERIC") != nullptr;
+  if (off || pl.nt != 256) return false;
+#define TVB_SHAPE(X, Y)                                  \
+  if (pl.wx == X && pl.wy == Y) {                        \
+    launch_nt<256, 2, X, Y>(grid, pl.smem, s, P, M);     \
+    return true;                                         \
+  }
+  TVB_SHAPE(23, 11)
+  TVB_SHAPE(25, 10)
+  TVB_SHAPE(28, 9)
+  TVB_SHAPE(42, 6)
+#undef TVB_SHAPE
+  return false;
 }
 
 cudaError_t launch_matvec(const MatvecPlan& pl, MatvecParams P, const Modal& M, cudaStream_t s) {
@@ -450,11 +470,16 @@ cudaError_t launch_matvec(const MatvecPlan& pl, MatvecParams P, const Modal& M, 
   static bool attr_set = false;
   if (!attr_set) {
     set_smem_attr<256, 2>(110 * 1024);
+    set_smem_attr<256, 2, 23, 11>(110 * 1024);
+    set_smem_attr<256, 2, 25, 10>(110 * 1024);
+    set_smem_attr<256, 2, 28, 9>(110 * 1024);
+    set_smem_attr<256, 2, 42, 6>(110 * 1024);
     set_smem_attr<384, 1>(220 * 1024);
     set_smem_attr<512, 1>(220 * 1024);
     attr_set = true;
   }
   dim3 grid(pl.nctas);
+  if (launch_fixed_shape(pl, grid, s, P, M)) return cudaGetLastError();
   if (pl.nt == 256) launch_nt<256, 2>(grid, pl.smem, s, P, M);
   else if (pl.nt == 384) launch_nt<384, 1>(grid, pl.smem, s, P, M);
   else launch_nt<512, 1>(grid, pl.smem, s, P, M);

@@ -3,7 +3,7 @@
 // contain `check_every` complete iterations and reads back two ints per
 // launch; all scalars (alpha, beta, residual, stop flag) live on the device.
 //
-// Algorithm (identical to the reference, step for step):
+// Algorithm (the reference's, step for step; projection = 0):
 //   x0 = W E^-1 W^T f ; r = f - A x0 ; r[fixed] = 0 ; stop if |r|/|f_free| <= tol
 //   z = D^-1 r ; p = z - W E^-1 (AW)^T z ; rz = r.z
 //   loop: q = A p ; alpha = rz/(p.q) ; x += alpha p ; r -= alpha q
@@ -11,7 +11,7 @@
 //         p = z + beta p - W E^-1 (AW)^T z
 // with (AW)^T z evaluated as W^T (A z) (A symmetric, W zero on fixed DOFs).
 //
-// Stabilised projection: the loop projects z + beta p instead of z,
+// Stabilised projection (projection = 1, the Python default): the loop projects z + beta p instead of z,
 //     p = z + beta p - W E^-1 W^T (A z + beta q),   q = A p_old,
 // which equals the reference update in exact arithmetic (W^T A p_old = 0) but
 // re-imposes W^T A p = 0 every iteration. The reference recurrence lets that
@@ -424,7 +424,8 @@ int pcg_solve_multi(const PcgProblem& P, PcgResult* R, int* rstat, cudaStream_t 
         if ((e = launch_matvec(plan, mp, P.modal, cs)) != cudaSuccess) return e;
       }
       if (!(skip & 8) &&
-          (e = launch_restrict(A, P.nflags, D, W[c].t, W[c].yc, cs, stop, W[c].q, W[c].st)) != cudaSuccess)
+          (e = launch_restrict(A, P.nflags, D, W[c].t, W[c].yc, cs, stop, P.stabilized ? W[c].q : nullptr,
+                               W[c].st)) != cudaSuccess)
         return e;
     }
     if (!defl) return cudaSuccess;
@@ -460,7 +461,7 @@ int pcg_solve_multi(const PcgProblem& P, PcgResult* R, int* rstat, cudaStream_t 
       if (defl) {
         matvec(0, W[0].z, W[0].t, false, stop);
         cudaEventRecord(ev[3], s);
-        launch_restrict(A, P.nflags, D, W[0].t, W[0].yc, s, stop, W[0].q, W[0].st);
+        launch_restrict(A, P.nflags, D, W[0].t, W[0].yc, s, stop, P.stabilized ? W[0].q : nullptr, W[0].st);
         cudaEventRecord(ev[4], s);
         coarse_solve(0, 1, stop);
         cudaEventRecord(ev[5], s);

