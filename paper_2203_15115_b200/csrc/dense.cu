@@ -19,8 +19,8 @@
 //                     (fea.py:198) gathered from the block stencil, plus the
 //                     children's updates gathered through per-child position
 //                     maps (no atomics, fixed order)
-//   k_front_pivot     P = A_pp^-1 by a scalar sweep of the 64x64 pivot tile
-//                     in shared memory (pivots checked positive: SPD test)
+//   k_front_pivot     P = A_pp^-1 by a 2x2-block sweep of the 64x64 pivot
+//                     tile in registers (pivot blocks checked SPD)
 //   k_front_panel     CT_k = A_pk and R_k = P A_pk for every tile column k
 //   k_front_update    A_ik -= CT_i^T R_k on every lower tile (64x64x64 DFMA
 //                     tile GEMM, 8x4 register block per thread), and the
@@ -85,39 +85,69 @@ __global__ void __launch_bounds__(256) k_front_assemble(FrontFactor Fx, const in
   }
 }
 
-// P = A_pp^-1 of every front of the level that still has pivot block p
+// P = A_pp^-1 of every front of the level that still has pivot block p:
+// a sweep of the 64x64 pivot tile in 2x2 pivot blocks (32 steps). Thread t
+// keeps the 16 entries (rows t/64 + 4q, column t%64) in registers; per step
+// only the two pivot columns and rows travel through double-buffered shared
+// arrays, so a step costs one barrier. Pivot blocks are checked SPD.
 __global__ void __launch_bounds__(256) k_front_pivot(FrontFactor Fx, const int* fronts, int p) {
-  __shared__ double a[kFT][kFT + 1];
+  __shared__ double2 colb[2][kFT];  // a[i][k], a[i][k+1]
+  __shared__ double rowb[2][2][kFT];  // a[k][j], a[k+1][j]
   const FrontRec R = Fx.fronts[fronts[blockIdx.x]];
   if ((long long)p * kFT >= R.s_pad) return;
   const double* A = Fx.pool + R.a_off + (long long)p * kFT * R.nf + (long long)p * kFT;
   const int t = threadIdx.x, j = t % kFT, i0 = t / kFT;  // rows i0 + 4q, column j
-  for (int q = 0; q < 16; ++q) a[i0 + 4 * q][j] = A[(long long)(i0 + 4 * q) * R.nf + j];
-  __syncthreads();
-  bool bad = false;
-  for (int k = 0; k < kFT; ++k) {
-    const double d = a[k][k];
-    bad = bad || !(d > 0.0) || !isfinite(d);
-    const double pv = 1.0 / d;
-    const double akj = a[k][j];
-    double nv[16];
+  double v[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] = A[(long long)(i0 + 4 * q) * R.nf + j];
+  auto publish = [&](int k, int b) {  // pivot columns / rows k, k+1 into buffer b
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       const int i = i0 + 4 * q;
-      const double aik = a[i][k], aij = a[i][j];
-      if (i != k && j != k) nv[q] = fma(-aik * pv, akj, aij);
-      else if (i != k) nv[q] = aik * pv;   // j == k
-      else if (j != k) nv[q] = pv * akj;   // i == k
-      else nv[q] = -pv;
+      if (j == k) colb[b][i].x = v[q];
+      if (j == k + 1) colb[b][i].y = v[q];
+      if (i == k) rowb[b][0][j] = v[q];
+      if (i == k + 1) rowb[b][1][j] = v[q];
     }
-    __syncthreads();
+  };
+  publish(0, 0);
+  __syncthreads();
+  bool bad = false;
+  for (int k = 0; k < kFT; k += 2) {
+    const int b = (k >> 1) & 1;
+    const double2 pk = colb[b][k], pk1 = colb[b][k + 1];  // (a_kk, a_k,k+1), (a_k+1,k, a_k+1,k+1)
+    const double det = pk.x * pk1.y - pk.y * pk1.x;
+    bad = bad || !(pk.x > 0.0) || !(det > 0.0) || !isfinite(det);
+    const double id = 1.0 / det;
+    const double p00 = pk1.y * id, p01 = -pk.y * id, p10 = -pk1.x * id, p11 = pk.x * id;  // inv 2x2
+    const double rk = rowb[b][0][j], rk1 = rowb[b][1][j];
+    // (P [a_kj; a_k+1,j]) for this column
+    const double w0 = p00 * rk + p01 * rk1, w1 = p10 * rk + p11 * rk1;
+    const bool jk = j == k || j == k + 1;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) a[i0 + 4 * q][j] = nv[q];
+    for (int q = 0; q < 16; ++q) {
+      const int i = i0 + 4 * q;
+      const bool ik = i == k || i == k + 1;
+      const double2 c = colb[b][i];
+      double nv;
+      if (!ik && !jk) {
+        nv = fma(-c.x, w0, fma(-c.y, w1, v[q]));
+      } else if (!ik) {  // column k or k+1: [a_ik a_ik+1] P
+        nv = j == k ? c.x * p00 + c.y * p10 : c.x * p01 + c.y * p11;
+      } else if (!jk) {  // row k or k+1: P [a_kj; a_k+1,j]
+        nv = i == k ? w0 : w1;
+      } else {
+        nv = -(i == k ? (j == k ? p00 : p01) : (j == k ? p10 : p11));
+      }
+      v[q] = nv;
+    }
+    if (k + 2 < kFT) publish(k + 2, b ^ 1);
     __syncthreads();
   }
-  if (bad && j == 0 && i0 == 0) atomicOr(Fx.d_err, 1);
+  if (bad && t == 0) atomicOr(Fx.d_err, 1);
   double* P = Fx.scratch + R.scr_off;
-  for (int q = 0; q < 16; ++q) P[(i0 + 4 * q) * kFT + j] = -a[i0 + 4 * q][j];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) P[(i0 + 4 * q) * kFT + j] = -v[q];
 }
 
 // smem[m * ldb + b] = tile element (row m, col b) of the pivot row block A_pk

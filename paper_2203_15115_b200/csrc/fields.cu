@@ -227,10 +227,17 @@ __device__ __forceinline__ unsigned long long okey(double v) {
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-// state: [0] prefix key bits, [1] prefix mask, [2] k remaining, [3] count greater
-__global__ void k_radix_hist(const double* ls, const uint8_t* design, long long n, const unsigned long long* state,
-                             int shift, unsigned int* hist) {
+// state: [0] prefix key bits, [1] prefix mask, [2] k remaining, [3] count greater.
+// One launch per 8-bit digit: every CTA adds its histogram of the candidates
+// (keys matching the prefix so far); the last CTA to finish (done counter)
+// picks the digit holding the k-th largest key, extends the prefix, and
+// clears the histogram and the counter for the next digit -- no separate
+// single-CTA pick launch (round 1: 8 x 7-16 us of launch-latency-bound picks).
+__global__ void __launch_bounds__(256) k_radix_hist(const double* ls, const uint8_t* design, long long n,
+                                                    unsigned long long* state, int shift, unsigned int* hist,
+                                                    unsigned int* done) {
   __shared__ unsigned int sh[256];
+  __shared__ bool last;
   for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   const unsigned long long pref = state[0], mask = state[1];
@@ -243,26 +250,33 @@ __global__ void k_radix_hist(const double* ls, const uint8_t* design, long long 
   __syncthreads();
   for (int i = threadIdx.x; i < 256; i += blockDim.x)
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
-}
-
-// choose the digit holding the k-th largest (descending), update state, clear hist
-__global__ void k_radix_pick(unsigned long long* state, int shift, unsigned int* hist) {
-  if (threadIdx.x != 0) return;
-  unsigned long long kr = state[2];
-  unsigned long long gt = state[3];
-  int d = 255;
-  for (; d >= 0; --d) {
-    const unsigned long long c = hist[d];
-    if (c >= kr) break;
-    kr -= c;
-    gt += c;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    sh[i] = atomicAdd(&hist[i], 0u);  // L2-coherent read of the completed histogram
+    hist[i] = 0u;
   }
-  if (d < 0) d = 0;
-  state[0] |= ((unsigned long long)d) << shift;
-  state[1] |= 255ull << shift;
-  state[2] = kr;
-  state[3] = gt;
-  for (int i = 0; i < 256; ++i) hist[i] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long kr = state[2], gt = state[3];
+    int d = 255;
+    for (; d >= 0; --d) {
+      const unsigned long long c = sh[d];
+      if (c >= kr) break;
+      kr -= c;
+      gt += c;
+    }
+    if (d < 0) d = 0;
+    state[0] = pref | ((unsigned long long)d) << shift;
+    state[1] = mask | 255ull << shift;
+    state[2] = kr;
+    state[3] = gt;
+    *done = 0u;
+  }
 }
 
 // per-block count of design elements whose key equals the threshold key
@@ -448,15 +462,13 @@ cudaError_t launch_select(const double* ls, const uint8_t* design, long long n, 
   const unsigned long long init[4] = {0ull, 0ull, (unsigned long long)(k > 0 ? k : 1), 0ull};
   cudaError_t e = cudaMemcpyAsync(state, init, sizeof(init), cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(hist, 0, 256 * sizeof(unsigned int), s);
+  unsigned int* done = (unsigned int*)((char*)ws + 32);
+  e = cudaMemsetAsync(done, 0, 32 + 256 * sizeof(unsigned int), s);  // counter and histogram
   if (e != cudaSuccess) return e;
   int nbh = (int)((n + 255) / 256);
   if (nbh > 1184) nbh = 1184;
   if (nbh < 1) nbh = 1;
-  for (int shift = 56; shift >= 0; shift -= 8) {
-    k_radix_hist<<<nbh, 256, 0, s>>>(ls, design, n, state, shift, hist);
-    k_radix_pick<<<1, 32, 0, s>>>(state, shift, hist);
-  }
+  for (int shift = 56; shift >= 0; shift -= 8) k_radix_hist<<<nbh, 256, 0, s>>>(ls, design, n, state, shift, hist, done);
   const int nb = (int)((n + 1023) / 1024);
   if (k <= 0) {
     // nothing retained: threshold above every key
