@@ -819,7 +819,7 @@ int tvb_element_state(int nx, int ny, int nz, double h, double E, double nu, con
     A.pnorm_partials = (double*)d_ws;
   }
   if (int st = check(launch_element_state(A, s))) return st;
-  if (d_pn_sums) return check(launch_sum_pairs((const double*)d_ws, elem_grid(A.g.ne), d_pn_sums, s));
+  if (d_pn_sums) return check(launch_sum_pairs((const double*)d_ws, elem_state_ctas(A.g), d_pn_sums, s));
   return kStatusOk;
 }
 

@@ -13,6 +13,8 @@
 // All element maps are HBM-bound streaming kernels: one thread per element,
 // the 8 corner nodes gathered from the interleaved node vector (neighbouring
 // threads share nodes through L1/L2).
+#include <cstdlib>
+
 #include "fields.cuh"
 #include "vec.cuh"
 
@@ -85,6 +87,133 @@ __device__ __forceinline__ double powi(double x, int p) {
     p >>= 1;
   }
   return r;
+}
+
+// ---- z-marching element maps --------------------------------------------
+// Thread = one element column segment (ex, ey, [z0, z1)); consecutive threads
+// take consecutive ex. The centroid gradient splits into face sums,
+//   d/dx = Sx(bottom) + Sx(top), d/dy = Sy(bottom) + Sy(top), d/dz = S(top) - S(bottom)
+// (Sx = sum of +-u over the face's 4 nodes by x side, S = plain sum), so each
+// element loads only its top face (4 nodes) and reuses the bottom face of
+// the element below: half the gather loads and index math of the one-
+// element-per-thread form. Segments are sized to give ~2 waves of threads.
+struct FaceSums {
+  double sx[3], sy[3], s[3];
+};
+
+__device__ __forceinline__ void face_sums(const Grid& G, const double* __restrict__ u, int ex, int ey, int z,
+                                          FaceSums& F) {
+  const long long n00 = G.node(ex, ey, z), n01 = n00 + G.px;
+  double v[4][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    v[0][a] = __ldg(u + 3 * n00 + a);
+    v[1][a] = __ldg(u + 3 * n00 + 3 + a);
+    v[2][a] = __ldg(u + 3 * n01 + a);
+    v[3][a] = __ldg(u + 3 * n01 + 3 + a);
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    F.sx[a] = (v[1][a] - v[0][a]) + (v[3][a] - v[2][a]);
+    F.sy[a] = (v[2][a] - v[0][a]) + (v[3][a] - v[1][a]);
+    F.s[a] = (v[0][a] + v[1][a]) + (v[2][a] + v[3][a]);
+  }
+}
+
+__device__ __forceinline__ void strain_of_faces(const FaceSums& B, const FaceSums& T, double inv4h,
+                                                double (&eps)[6]) {
+  const double gx0 = B.sx[0] + T.sx[0], gx1 = B.sx[1] + T.sx[1], gx2 = B.sx[2] + T.sx[2];
+  const double gy0 = B.sy[0] + T.sy[0], gy1 = B.sy[1] + T.sy[1], gy2 = B.sy[2] + T.sy[2];
+  const double gz0 = T.s[0] - B.s[0], gz1 = T.s[1] - B.s[1], gz2 = T.s[2] - B.s[2];
+  eps[0] = gx0 * inv4h;
+  eps[1] = gy1 * inv4h;
+  eps[2] = gz2 * inv4h;
+  eps[3] = (gy0 + gx1) * inv4h;
+  eps[4] = (gz1 + gy2) * inv4h;
+  eps[5] = (gz0 + gx2) * inv4h;
+}
+
+// segment length along z so that nx * ny * ceil(nz / L) threads make ~2 waves
+__host__ __device__ inline int march_len(const Grid& G) {
+  const long long cols = (long long)G.nx * G.ny;
+  const long long want = 148LL * 2048;
+  long long seg = (want + cols - 1) / cols;  // segments per column
+  if (seg < 1) seg = 1;
+  if (seg > G.nz) seg = G.nz;
+  return (int)((G.nz + seg - 1) / seg);
+}
+
+__host__ __device__ inline long long march_threads(const Grid& G) {
+  const int L = march_len(G);
+  return (long long)G.nx * G.ny * ((G.nz + L - 1) / L);
+}
+
+#define TVB_MARCH_BEGIN(G)                                                        \
+  const int L = march_len(G);                                                     \
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;         \
+  const long long cols = (long long)(G).nx * (G).ny;                              \
+  const bool live = tid < march_threads(G);                                       \
+  const int ex = (int)(tid % (G).nx), ey = (int)((tid / (G).nx) % (G).ny);        \
+  const int z0 = (int)(tid / cols) * L, z1 = min((G).nz, z0 + L);
+
+__global__ void __launch_bounds__(256) k_element_state_z(ElemArgs A) {
+  __shared__ double red[32];
+  const Grid& G = A.g;
+  TVB_MARCH_BEGIN(G)
+  double pn = 0.0, oc = 0.0;
+  if (live) {
+    FaceSums Fb, Ft;
+    face_sums(G, A.u, ex, ey, z0, Fb);
+    for (int z = z0; z < z1; ++z) {
+      face_sums(G, A.u, ex, ey, z + 1, Ft);
+      const long long e = G.elem(ex, ey, z);
+      double eps[6], sig[6];
+      strain_of_faces(Fb, Ft, A.inv4h, eps);
+      const double occ = A.occ[e];
+      stress_of(A.D, occ, eps, sig);
+      const double vm = vm_of(sig);
+      if (A.strains)
+        for (int i = 0; i < 6; ++i) A.strains[6 * e + i] = eps[i];
+      if (A.stresses)
+        for (int i = 0; i < 6; ++i) A.stresses[6 * e + i] = sig[i];
+      if (A.vm) A.vm[e] = vm;
+      if (A.tj) A.tj[e] = sens_of(A.D, sig, eps);
+      if (A.pnorm_partials) {
+        pn += occ * powi(vm, A.p);
+        oc += occ;
+      }
+      Fb = Ft;
+    }
+  }
+  if (A.pnorm_partials) {
+    pn = block_sum(pn, red);
+    oc = block_sum(oc, red);
+    if (threadIdx.x == 0) {
+      A.pnorm_partials[2 * blockIdx.x] = pn;
+      A.pnorm_partials[2 * blockIdx.x + 1] = oc;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_stress_sens_z(ElemArgs A, const double* lam, double* ts) {
+  const Grid& G = A.g;
+  TVB_MARCH_BEGIN(G)
+  if (!live) return;
+  FaceSums Ub, Ut, Lb, Lt;
+  face_sums(G, A.u, ex, ey, z0, Ub);
+  face_sums(G, lam, ex, ey, z0, Lb);
+  for (int z = z0; z < z1; ++z) {
+    face_sums(G, A.u, ex, ey, z + 1, Ut);
+    face_sums(G, lam, ex, ey, z + 1, Lt);
+    const long long e = G.elem(ex, ey, z);
+    double eu[6], sig[6], el[6];
+    strain_of_faces(Ub, Ut, A.inv4h, eu);
+    stress_of(A.D, A.occ[e], eu, sig);
+    strain_of_faces(Lb, Lt, A.inv4h, el);
+    ts[e] = sens_of(A.D, sig, el);
+    Ub = Ut;
+    Lb = Lt;
+  }
 }
 
 __global__ void k_element_state(ElemArgs A) {
@@ -397,13 +526,18 @@ cudaError_t launch_casting_project(const Grid& G, int axis, int P, const double*
 
 int elem_grid(long long n) { return (int)((n + 255) / 256); }
 
+// CTAs of the element-state launch (= number of p-norm partial pairs)
+int elem_state_ctas(const Grid& G) { return (int)((march_threads(G) + 255) / 256); }
+
 cudaError_t launch_element_state(const ElemArgs& A, cudaStream_t s) {
-  k_element_state<<<elem_grid(A.g.ne), 256, 0, s>>>(A);
+  if (getenv("TVB_ELEM_FLAT")) k_element_state<<<elem_grid(A.g.ne), 256, 0, s>>>(A);  // A/B only
+  else k_element_state_z<<<elem_state_ctas(A.g), 256, 0, s>>>(A);
   return cudaGetLastError();
 }
 
 cudaError_t launch_stress_sens(const ElemArgs& A, const double* lam, double* ts, cudaStream_t s) {
-  k_stress_sens<<<elem_grid(A.g.ne), 256, 0, s>>>(A, lam, ts);
+  if (getenv("TVB_ELEM_FLAT")) k_stress_sens<<<elem_grid(A.g.ne), 256, 0, s>>>(A, lam, ts);
+  else k_stress_sens_z<<<elem_state_ctas(A.g), 256, 0, s>>>(A, lam, ts);
   return cudaGetLastError();
 }
 

@@ -33,6 +33,7 @@ struct CombineArgs {
 };
 
 int elem_grid(long long n);
+int elem_state_ctas(const Grid& G);
 cudaError_t launch_element_state(const ElemArgs& A, cudaStream_t s);
 cudaError_t launch_stress_sens(const ElemArgs& A, const double* lam, double* ts, cudaStream_t s);
 // sums: device [2] = (sum occ vm^p, sum occ)

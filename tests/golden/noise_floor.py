@@ -109,8 +109,9 @@ class NoisyOp(RefOp):
     def __init__(self, op, seed=0):
         super().__init__(op)
         self.rng = np.random.default_rng(seed)
+        self.apply = self.noisy_apply
 
-    def apply(self, u):
+    def noisy_apply(self, u):
         y = self.op.apply(u)
         return y * (1.0 + 2.0 ** -53 * self.rng.standard_normal(y.size))
 
