@@ -31,7 +31,10 @@ OFFS = np.array([[0, 0, 0], [1, 0, 0], [1, 1, 0], [0, 1, 0],
 
 
 class FastDeflation:
-    def __init__(self, nx, ny, nz, h, occ, fixed_dofs, block, k0, design_mask=None, origin=(0.0, 0.0, 0.0)):
+    def __init__(self, nx, ny, nz, h, occ, fixed_dofs, block, k0, design_mask=None, origin=(0.0, 0.0, 0.0),
+                 reverse=False):
+        """reverse=True (rounding studies only, tests/golden/noise_floor.py):
+        accumulate the KW columns over the near elements in descending order."""
         if block < 2:
             raise ValueError("agglomerate side must be >= 2")
         self.dims = (nx, ny, nz)
@@ -116,6 +119,8 @@ class FastDeflation:
                     ye = s[:, None, None] * np.einsum("ab,ebk->eak", k0, ue)
                     ye[s == 0.0] = 0.0
                     out = np.zeros_like(wl)
+                    if reverse:
+                        ed, ye = ed[::-1], ye[::-1]
                     np.add.at(out, ed.ravel(), ye.reshape(-1, k))     # element-ascending accumulation
                     # global dofs of the local node box; Dirichlet rows zeroed (fea.py:73-75)
                     LZ, LY, LX = np.meshgrid(np.arange(ez0, ez1 + 2), np.arange(ey0, ey1 + 2),

@@ -13,6 +13,7 @@
 // All element maps are HBM-bound streaming kernels: one thread per element,
 // the 8 corner nodes gathered from the interleaved node vector (neighbouring
 // threads share nodes through L1/L2).
+#include <algorithm>
 #include <cstdlib>
 
 #include "fields.cuh"
@@ -213,6 +214,97 @@ __global__ void __launch_bounds__(256) k_stress_sens_z(ElemArgs A, const double*
     ts[e] = sens_of(A.D, sig, el);
     Ub = Ut;
     Lb = Lt;
+  }
+}
+
+// h_e (see k_adjoint_h) on element column segments, face sums reused
+__global__ void __launch_bounds__(256) k_adjoint_h_z(ElemArgs A, const double* sums, double* h6) {
+  const Grid& G = A.g;
+  TVB_MARCH_BEGIN(G)
+  if (!live) return;
+  const double S = sums[0] / sums[1];
+  const double inv_occ_sum = 1.0 / sums[1];
+  const double sp = pow(S, 1.0 / A.p - 1.0);
+  FaceSums Fb, Ft;
+  face_sums(G, A.u, ex, ey, z0, Fb);
+  for (int z = z0; z < z1; ++z) {
+    face_sums(G, A.u, ex, ey, z + 1, Ft);
+    const long long e = G.elem(ex, ey, z);
+    double eps[6], sig[6];
+    strain_of_faces(Fb, Ft, A.inv4h, eps);
+    const double occ = A.occ[e];
+    stress_of(A.D, occ, eps, sig);
+    const double vm = vm_of(sig);
+    const double coef = sp * (occ * inv_occ_sum) * powi(vm, A.p - 2) * occ;
+    double qs[6];
+    qs[0] = sig[0] - 0.5 * (sig[1] + sig[2]);
+    qs[1] = sig[1] - 0.5 * (sig[0] + sig[2]);
+    qs[2] = sig[2] - 0.5 * (sig[0] + sig[1]);
+    qs[3] = 3.0 * sig[3];
+    qs[4] = 3.0 * sig[4];
+    qs[5] = 3.0 * sig[5];
+    double out[6];
+    stress_of(A.D, coef, qs, out);
+    double2* h2 = reinterpret_cast<double2*>(h6 + 6 * e);
+    h2[0] = make_double2(out[0], out[1]);
+    h2[1] = make_double2(out[2], out[3]);
+    h2[2] = make_double2(out[4], out[5]);
+    Fb = Ft;
+  }
+}
+
+// rhs on node column segments: the node at (x, y, z) sums the B_c^T h of its
+// 8 elements; the 4 elements of layer z-1 were the "upper" layer of the
+// previous node, so each step loads one element layer (4 x 6 doubles).
+__global__ void __launch_bounds__(256) k_adjoint_gather_z(Grid G, double inv4h, const double* h6,
+                                                          const uint8_t* nflags, double* rhs) {
+  const long long cols = (long long)G.px * G.py;
+  const long long seg = (148LL * 2048 + cols - 1) / cols;
+  const int L = (int)((G.pz + min(seg, (long long)G.pz) - 1) / min(seg, (long long)G.pz));
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long nseg = (G.pz + L - 1) / L;
+  if (tid >= cols * nseg) return;
+  const int x = (int)(tid % G.px), y = (int)((tid / G.px) % G.py);
+  const int z0 = (int)(tid / cols) * L, z1 = min(G.pz, z0 + L);
+  // per element layer: contribution to this node from the 4 elements (dx, dy) in {-1,0}^2 of that layer,
+  // split by the node's local z side (oz = 0: the node is on the element's bottom face)
+  auto layer = [&](int ez, double (&bot)[3], double (&top)[3]) {
+    // bot: node on the bottom face of layer ez (sz = -1); top: node on its top face (sz = +1)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) bot[a] = top[a] = 0.0;
+    if (ez < 0 || ez >= G.nz) return;
+#pragma unroll
+    for (int dy = -1; dy <= 0; ++dy)
+#pragma unroll
+      for (int dx = -1; dx <= 0; ++dx) {
+        const int ex = x + dx, ey = y + dy;
+        if (ex < 0 || ex >= G.nx || ey < 0 || ey >= G.ny) continue;
+        const double* h = h6 + 6 * G.elem(ex, ey, ez);
+        const double2 h01 = __ldg(reinterpret_cast<const double2*>(h));
+        const double2 h23 = __ldg(reinterpret_cast<const double2*>(h) + 1);
+        const double2 h45 = __ldg(reinterpret_cast<const double2*>(h) + 2);
+        const double sx = dx ? 1.0 : -1.0, sy = dy ? 1.0 : -1.0;
+        // terms without sz, and the sz coefficients
+        const double r0 = sx * h01.x + sy * h23.y, c0 = h45.y;
+        const double r1 = sy * h01.y + sx * h23.y, c1 = h45.x;
+        const double r2 = sy * h45.x + sx * h45.y, c2 = h23.x;
+        bot[0] += r0 - c0; top[0] += r0 + c0;
+        bot[1] += r1 - c1; top[1] += r1 + c1;
+        bot[2] += r2 - c2; top[2] += r2 + c2;
+      }
+  };
+  double lowTop[3], lowBot[3], upBot[3], upTop[3];
+  layer(z0 - 1, lowBot, lowTop);  // the node is on the TOP face of layer z - 1
+  for (int z = z0; z < z1; ++z) {
+    layer(z, upBot, upTop);        // ... and on the BOTTOM face of layer z
+    const long long n = G.node(x, y, z);
+    const uint8_t fl = nflags ? nflags[n] : 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double r = (upBot[a] + lowTop[a]) * inv4h;
+      rhs[3 * n + a] = ((fl >> a) & 1) ? 0.0 : r;
+      lowTop[a] = upTop[a];
+    }
   }
 }
 
@@ -543,8 +635,18 @@ cudaError_t launch_stress_sens(const ElemArgs& A, const double* lam, double* ts,
 
 cudaError_t launch_adjoint(const ElemArgs& A, const double* sums, double* h6, const uint8_t* nflags, double* rhs,
                            cudaStream_t s) {
-  k_adjoint_h<<<elem_grid(A.g.ne), 256, 0, s>>>(A, sums, h6);
-  k_adjoint_gather<<<(unsigned)((A.g.nn + 255) / 256), 256, 0, s>>>(A.g, A.inv4h, h6, nflags, rhs);
+  if (getenv("TVB_ELEM_FLAT")) {  // A/B only
+    k_adjoint_h<<<elem_grid(A.g.ne), 256, 0, s>>>(A, sums, h6);
+    k_adjoint_gather<<<(unsigned)((A.g.nn + 255) / 256), 256, 0, s>>>(A.g, A.inv4h, h6, nflags, rhs);
+    return cudaGetLastError();
+  }
+  k_adjoint_h_z<<<elem_state_ctas(A.g), 256, 0, s>>>(A, sums, h6);
+  const Grid& G = A.g;
+  const long long cols = (long long)G.px * G.py;
+  const long long seg = std::min((148LL * 2048 + cols - 1) / cols, (long long)G.pz);
+  const long long L = (G.pz + seg - 1) / seg;
+  const long long nthr = cols * ((G.pz + L - 1) / L);
+  k_adjoint_gather_z<<<(unsigned)((nthr + 255) / 256), 256, 0, s>>>(G, A.inv4h, h6, nflags, rhs);
   return cudaGetLastError();
 }
 
