@@ -143,9 +143,6 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
   double* red = Xc + 2 * XS;
   // [kStage][NT] staging lists: (smem byte offset, in-plane global byte offset)
   int2* st_list = reinterpret_cast<int2*>(red + NT / 32 + 1);
-  // one dummy double per thread (target of the zero-byte copies), as a byte offset from Up
-  const int dummy_off = (int)((reinterpret_cast<char*>(st_list + kStage * NT) - reinterpret_cast<char*>(Up)) +
-                              8 * threadIdx.x);
 
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
@@ -209,8 +206,6 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
           const int jy = jy_lo + i / rw, r = r_lo + i % rw;
           st_list[q * NT + t] = make_int2(8 * (jy * S + r), 8 * (3 * G.px * (y0 - 1 + jy) + 3 * (x0 - 1) + r));
           ncnt = q + 1;
-        } else {  // unused entry: a zero-byte copy into this thread's dummy slot
-          st_list[q * NT + t] = make_int2(dummy_off, 0);
         }
       }
     }
@@ -229,26 +224,29 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
     }
     const unsigned up_s = (unsigned)__cvta_generic_to_shared(Up), oc_s = (unsigned)__cvta_generic_to_shared(Oc);
 
-    // stage node plane k and occupancy layer k into ring slot sl: branch-free,
-    // every list entry is one cp.async whose source size is 8 bytes in the
-    // grid and 0 (zero fill) for the halo planes above / below it; unused
-    // entries copy zero bytes into the thread's dummy slot
+    // stage node plane k and occupancy layer k into ring slot sl (zero-filled outside the grid)
     auto load_layer = [&](int k, int sl) {
-      const bool kin = k >= 0 && k < G.pz;
-      const char* src = reinterpret_cast<const char*>(kin ? P.u + plane_stride * k : P.u);
-      const unsigned nb = kin ? 8u : 0u;
-      const unsigned base = up_s + (unsigned)(8 * sl * PS);
-      int2 e[kStage];
+      if (k >= 0 && k < G.pz) {
+        const char* src = reinterpret_cast<const char*>(P.u + plane_stride * k);
+        const unsigned base = up_s + (unsigned)(8 * sl * PS);
+        // all list entries first (unused slots are read but never followed),
+        // then the predicated copies: no LDS -> LDGSTS pairs in the stream
+        int2 e[kStage];
 #pragma unroll
-      for (int q = 0; q < kStage; ++q) e[q] = st_list[q * NT + t];
+        for (int q = 0; q < kStage; ++q) e[q] = st_list[q * NT + t];
 #pragma unroll
-      for (int q = 0; q < kStage; ++q) {
-        const bool real = q < ncnt;
-        cp_async8_zfill(real ? base + (unsigned)e[q].x : up_s + (unsigned)e[q].x, src + e[q].y, real ? nb : 0u);
+        for (int q = 0; q < kStage; ++q)
+          if (q < ncnt) cp_async8_s(base + (unsigned)e[q].x, src + e[q].y);
+      } else {  // halo plane above / below the grid (first / last piece only)
+        double* dst = Up + sl * PS;
+#pragma unroll
+        for (int q = 0; q < kStage; ++q)
+          if (q < ncnt) dst[st_list[q * NT + t].x / 8] = 0.0;
       }
-      const bool oin = has_occ && k >= 0 && k < G.nz;
-      cp_async8_zfill(has_occ ? oc_s + (unsigned)(8 * sl * OS) + ooff : up_s + (unsigned)dummy_off,
-                      oin ? (const void*)(P.occ + layer_stride * k + oeoff) : (const void*)P.occ, oin ? 8u : 0u);
+      if (has_occ) {
+        if (k >= 0 && k < G.nz) cp_async8_s(oc_s + (unsigned)(8 * sl * OS) + ooff, P.occ + layer_stride * k + oeoff);
+        else Oc[sl * OS + ooff / 8] = 0.0;
+      }
       cp_async_commit();
     };
 
@@ -380,7 +378,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
 static size_t matvec_smem(int nt, int wx, int wy) {
   const int PS = (wy + 1) * plane_row_stride(wx);
   return sizeof(double) * (kRing * (size_t)PS + kRing * (size_t)wx * wy + 1 + 2 * kXw * (size_t)(nt + kXcPad) + nt / 32 + 1) +
-         2 * sizeof(int) * kStage * (size_t)nt + sizeof(double) * (size_t)nt;
+         2 * sizeof(int) * kStage * (size_t)nt;
 }
 
 static int ctas_per_sm(int nt) { return nt == 256 ? 2 : 1; }
