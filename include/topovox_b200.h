@@ -256,6 +256,10 @@ typedef struct tvb_pcg_desc {
    *   1 = stabilised:               p = z + beta p - W E^-1 W^T (A z + beta A p_old),
    *       which re-imposes W^T A p = 0 every iteration (robust at tol ~1e-12) */
   int projection;
+  /* node flags (fixed axes + structural bit) the deflation space was built
+   * with (restriction / prolongation); NULL -> d_nflags. The reference builds
+   * W from the deflation space's own Dirichlet set and topology (fea.py:113-183) */
+  const uint8_t* d_defl_nflags;
   /* outputs */
   int iterations;
   double residual;

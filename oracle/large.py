@@ -152,14 +152,52 @@ class FastDeflation:
         E = (self.W.T @ self.KW).tocsc()
         return (0.5 * (E + E.T)).tocsc()
 
-    def prepare(self, op=None) -> None:
+    def prepare(self, op=None, direct=True) -> None:
+        """direct: sparse LU of E. direct=False (C2(b)/C5 fixtures, where
+        SuperLU's fill makes the LU impractical): conjugate gradients on E
+        (cond(E) ~ 10 for these rigid-mode coarse operators) iterated until
+        the residual stops decreasing -- exact to a few units of rounding."""
         if self.W is None or self._lu is not None:
             return
         self.E = self.coarse_matrix()
-        self._lu = scipy.sparse.linalg.splu(self.E, permc_spec="MMD_AT_PLUS_A")
+        if direct:
+            self._lu = scipy.sparse.linalg.splu(self.E, permc_spec="MMD_AT_PLUS_A")
+        else:
+            self._lu = "cg"
+            self._dinv = 1.0 / self.E.diagonal()
+
+    def _cg(self, b):
+        E, dinv = self.E, self._dinv
+        x = np.zeros_like(b)
+        r = b.copy()
+        z = dinv * r
+        p = z.copy()
+        rz = r @ z
+        best = np.inf
+        stall = 0
+        for _ in range(2000):
+            q = E @ p
+            a = rz / (p @ q)
+            x += a * p
+            r -= a * q
+            rn = np.linalg.norm(r)
+            if rn < best * 0.5:
+                best, stall = rn, 0
+            else:
+                stall += 1
+            if stall >= 20 or rn == 0.0:
+                break
+            z = dinv * r
+            rz_new = r @ z
+            p = z + (rz_new / rz) * p
+            rz = rz_new
+        return x
 
     def coarse_solve(self, rhs):
-        return self._lu.solve(np.asarray(rhs, dtype=float))
+        rhs = np.asarray(rhs, dtype=float)
+        if isinstance(self._lu, str):
+            return self._cg(rhs)
+        return self._lu.solve(rhs)
 
 
 def sparse_coarse_solver(E_dense_or_sparse):

@@ -58,7 +58,7 @@ class PcgDesc(ctypes.Structure):
         ("tol", c_double), ("max_iters", c_int), ("check_every", c_int),
         ("block", c_int), ("d_cen", P), ("d_S", P), ("d_keep", P),
         ("d_coarse", P), ("coarse_kind", c_int), ("coarse_nd", ctypes.POINTER(CoarseND)),
-        ("projection", c_int),
+        ("projection", c_int), ("d_defl_nflags", P),
         ("iterations", c_int), ("residual", c_double), ("fnorm", c_double),
     ]
 

@@ -664,6 +664,7 @@ static int pcg_problem(const tvb_pcg_desc* d, PcgProblem& P) {
   P.coarse_kind = d->coarse_kind;
   if (d->projection != 0 && d->projection != 1) return kStatusBadArg;
   P.stabilized = d->projection == 1;
+  P.dflags = d->d_defl_nflags ? d->d_defl_nflags : d->d_nflags;
   if (P.coarse_kind == 1) {
     if (!d->coarse_nd) return kStatusBadArg;
     P.nd = coarse_nd_dev(d->coarse_nd);

@@ -231,7 +231,7 @@ int pcg_solve_multi(const PcgProblem& P, PcgResult* R, int* rstat, cudaStream_t 
   };
   auto coarse_project = [&](int c, const double* v) -> cudaError_t {
     // nu = S E^-1 W^T v  (prologue: v = f or A z)
-    cudaError_t e = launch_restrict(A, P.nflags, D, v, W[c].yc, s, nullptr, nullptr, W[c].st);
+    cudaError_t e = launch_restrict(A, P.dflags, D, v, W[c].yc, s, nullptr, nullptr, W[c].st);
     if (e != cudaSuccess) return e;
     if ((e = coarse_solve(c, 1, nullptr)) != cudaSuccess) return e;
     return launch_block_nu(A, D, W[c].mu, W[c].nu, s, nullptr);
@@ -298,7 +298,7 @@ int pcg_solve_multi(const PcgProblem& P, PcgResult* R, int* rstat, cudaStream_t 
     // x0
     if (defl) {
       TVB_CK(coarse_project(c, P.fs[c]));
-      TVB_CK(launch_prolong(A, P.nflags, D, W[c].nu, x, nullptr, nullptr, 0, s));
+      TVB_CK(launch_prolong(A, P.dflags, D, W[c].nu, x, nullptr, nullptr, 0, s));
     } else {
       TVB_CK(cudaMemsetAsync(x, 0, nd * sizeof(double), s));
     }
@@ -317,7 +317,7 @@ int pcg_solve_multi(const PcgProblem& P, PcgResult* R, int* rstat, cudaStream_t 
     if (defl) {
       TVB_CK(matvec(c, W[c].z, W[c].q, false, nullptr));
       TVB_CK(coarse_project(c, W[c].q));
-      TVB_CK(launch_prolong(A, P.nflags, D, W[c].nu, W[c].p, W[c].z, W[c].st, 2, s));
+      TVB_CK(launch_prolong(A, P.dflags, D, W[c].nu, W[c].p, W[c].z, W[c].st, 2, s));
     } else {
       TVB_CK(cudaMemcpyAsync(W[c].p, W[c].z, nd * sizeof(double), cudaMemcpyDeviceToDevice, s));
     }
@@ -424,7 +424,7 @@ int pcg_solve_multi(const PcgProblem& P, PcgResult* R, int* rstat, cudaStream_t 
         if ((e = launch_matvec(plan, mp, P.modal, cs)) != cudaSuccess) return e;
       }
       if (!(skip & 8) &&
-          (e = launch_restrict(A, P.nflags, D, W[c].t, W[c].yc, cs, stop, P.stabilized ? W[c].q : nullptr,
+          (e = launch_restrict(A, P.dflags, D, W[c].t, W[c].yc, cs, stop, P.stabilized ? W[c].q : nullptr,
                                W[c].st)) != cudaSuccess)
         return e;
     }
@@ -437,7 +437,7 @@ int pcg_solve_multi(const PcgProblem& P, PcgResult* R, int* rstat, cudaStream_t 
       const int* stop = &W[c].st->done;
       if ((e = launch_block_nu(A, D, W[c].mu, W[c].nu, sc(c), stop)) != cudaSuccess) return e;
       // p = z + beta p - W nu, and the deferred x += alpha p_old of this iteration
-      if ((e = launch_prolong(A, P.nflags, D, W[c].nu, W[c].p, W[c].z, W[c].st, 1, sc(c), P.xs[c])) != cudaSuccess)
+      if ((e = launch_prolong(A, P.dflags, D, W[c].nu, W[c].p, W[c].z, W[c].st, 1, sc(c), P.xs[c])) != cudaSuccess)
         return e;
     }
     return cudaSuccess;
@@ -461,12 +461,12 @@ int pcg_solve_multi(const PcgProblem& P, PcgResult* R, int* rstat, cudaStream_t 
       if (defl) {
         matvec(0, W[0].z, W[0].t, false, stop);
         cudaEventRecord(ev[3], s);
-        launch_restrict(A, P.nflags, D, W[0].t, W[0].yc, s, stop, P.stabilized ? W[0].q : nullptr, W[0].st);
+        launch_restrict(A, P.dflags, D, W[0].t, W[0].yc, s, stop, P.stabilized ? W[0].q : nullptr, W[0].st);
         cudaEventRecord(ev[4], s);
         coarse_solve(0, 1, stop);
         cudaEventRecord(ev[5], s);
         launch_block_nu(A, D, W[0].mu, W[0].nu, s, stop);
-        launch_prolong(A, P.nflags, D, W[0].nu, W[0].p, W[0].z, W[0].st, 1, s, P.xs[0]);
+        launch_prolong(A, P.dflags, D, W[0].nu, W[0].p, W[0].z, W[0].st, 1, s, P.xs[0]);
       } else {
         launch_pcg_pupdate(nd, W[0].p, W[0].z, W[0].st, s);
         for (int k = 3; k < 6; ++k) cudaEventRecord(ev[k], s);

@@ -28,7 +28,8 @@ struct PcgProblem {
   const int* keep;
   const double* coarse;  // dense inverse (coarse_kind 0)
   int coarse_kind;       // 0 dense inverse, 1 nested dissection
-  bool stabilized = false;  // projection of z + beta p (solver.cu header) instead of z
+  bool stabilized = false;
+  const uint8_t* dflags = nullptr;  // deflation space's node flags (restriction / prolongation)  // projection of z + beta p (solver.cu header) instead of z
   CoarseNDDev nd;
   const double* nd_factor = nullptr;  // L2-persisting window (the ND factor)
   size_t nd_factor_bytes = 0;

@@ -358,6 +358,31 @@ class DeflationSpace:
             sol = self.coarse_inv @ full
         return to_host_if(sol[mask], np_in)
 
+    def project_device(self, v):
+        """W E^-1 W^T v on device vectors (restriction, exact coarse solve,
+        prolongation kernels); the deflated-PCG projection of the reference's
+        ``project_out`` (fea.py:258-259) when v = K z."""
+        torch = _torch()
+        if self.coarse_inv is None and self.nd is None:
+            raise RuntimeError("DeflationSpace.prepare(op) must run first")
+        d = self.domain
+        nc = 6 * self.n_blocks
+        yc = torch.empty(nc, dtype=torch.float64, device="cuda")
+        check(lib().tvb_restrict(d.nx, d.ny, d.nz, self.block, d.h, ptr(self.nflags), ptr(self.cen), ptr(self.S),
+                                 ptr(self.keep), ptr(v), ptr(yc), stream_ptr()), "restrict")
+        if self.nd is not None:
+            ndi = torch.from_numpy(self.nd.nd_index()).cuda()
+            y = torch.empty_like(yc)
+            y[ndi] = yc
+            mu = self.nd.solve_device(y, torch.empty_like(yc))[ndi].contiguous()
+        else:
+            mu = (self.coarse_inv @ yc).contiguous()
+        out = torch.empty_like(v)
+        ws = torch.empty(nc, dtype=torch.float64, device="cuda")
+        check(lib().tvb_prolong(d.nx, d.ny, d.nz, self.block, d.h, ptr(self.nflags), ptr(self.cen), ptr(self.S),
+                                ptr(self.keep), ptr(mu), ptr(out), ptr(ws), stream_ptr()), "prolong")
+        return out
+
     # --- host views (compatibility / tests) ------------------------------------
     @property
     def W(self):
@@ -470,7 +495,8 @@ def solve_static(op: StiffnessOperator, f, tol: float = 1.0e-8, max_iters: int |
     if max_iters is None:
         max_iters = default_max_iters(op.n_dofs)
     if apply_op is not None or diag is not None:
-        res = _solve_generic(op, f_d, tol, max_iters, apply_op, diag)
+        defl = deflation if (deflation is not None and deflation.n_vectors > 0) else None
+        res = _solve_generic(op, f_d, tol, max_iters, apply_op, diag, defl)
         return SolveResult(to_host_if(res.u, np_in), res.iterations, res.residual)
     defl = deflation if (deflation is not None and deflation.n_vectors > 0) else None
     if defl is not None:
@@ -502,6 +528,7 @@ def _pcg_desc(op: StiffnessOperator, defl, tol: float, max_iters: int, check_eve
     if defl is not None:
         desc.block = defl.block
         desc.d_cen, desc.d_S, desc.d_keep = ptr(defl.cen), ptr(defl.S), ptr(defl.keep)
+        desc.d_defl_nflags = ptr(defl.nflags)  # W is the space's (its Dirichlet set / topology)
         if defl.nd is not None:
             desc.coarse_kind = 1
             desc.coarse_nd = ctypes.pointer(defl.nd.desc)
@@ -585,9 +612,12 @@ def solve_static_batch(op: StiffnessOperator, forces, tol: float = 1.0e-8, max_i
     return out
 
 
-def _solve_generic(op, f_d, tol, max_iters, apply_op, diag):
+def _solve_generic(op, f_d, tol, max_iters, apply_op, diag, defl=None):
     """PCG with a caller-supplied operator / diagonal (reference hook used for
-    shifted solves). Vector algebra on the device; no deflation."""
+    shifted solves, fea.py:218-299 with ``apply_op`` / ``diag``). Vector
+    algebra on the device. As in the reference, a deflation space still
+    deflates: it is prepared for ``op`` and projects with op's K (KW of
+    ``op``, fea.py:256-262), whatever ``apply_op`` is."""
     torch = _torch()
     free = torch.from_numpy(op.free_mask).cuda()
     A = apply_op if apply_op is not None else (lambda v: op.apply_device(v))
@@ -600,14 +630,22 @@ def _solve_generic(op, f_d, tol, max_iters, apply_op, diag):
         raise SingularSystem("zero stiffness diagonal on a loaded free DOF")
     inv_d = torch.zeros_like(f_d)
     inv_d[free] = 1.0 / dd[free]
-    x = torch.zeros_like(f_d)
-    r = f_d.clone()
+    if defl is not None:
+        defl.prepare(op)
+        x = defl.project_device(f_d.contiguous())  # W E^-1 W^T f
+        r = f_d - torch.as_tensor(A(x), device="cuda", dtype=torch.float64)
+
+        def project_out(v):
+            return defl.project_device(op.apply_device(v.contiguous()))
+    else:
+        x = torch.zeros_like(f_d)
+        r = f_d.clone()
     r[~free] = 0.0
     res = float(torch.linalg.norm(r)) / fnorm
     if res <= tol:
         return SolveResult(x, 0, res)
     z = inv_d * r
-    p = z.clone()
+    p = z - project_out(z) if defl is not None else z.clone()
     rz = float(r @ z)
     for it in range(1, max_iters + 1):
         q = torch.as_tensor(A(p), device="cuda", dtype=torch.float64)
@@ -620,6 +658,8 @@ def _solve_generic(op, f_d, tol, max_iters, apply_op, diag):
         z = inv_d * r
         rz_new = float(r @ z)
         p = z + (rz_new / rz) * p
+        if defl is not None:
+            p = p - project_out(z)
         rz = rz_new
     else:
         raise NoConvergence(f"CG did not reach {tol:g} in {max_iters} iterations (residual {res:.3e})",

@@ -15,7 +15,9 @@ What runs is the reference's own code except where it cannot finish:
   * deflation at C2(b)/C5: ``oracle.large.FastDeflation`` (the reference's
     basis/KW/E restated block-locally; the dense E would need 309 GB at
     C2(b)). It is checked below to be bitwise equal to the reference's
-    DeflationSpace (W, KW, E) on small grids and at C3;
+    DeflationSpace (W, KW, E) on small grids and at C3. Its coarse solve there
+    is CG on E run to the rounding floor (SuperLU's fill on these 3-D
+    stencils is impractical; cond(E) ~ 10);
   * loop: ``oracle.topovox_oracle.solve_static`` -- the reference's
     ``solve_static`` (fea.py:218-299) restated step for step, checked below to
     be bitwise equal to it -- with an observer that snapshots the iterate when
@@ -119,9 +121,9 @@ def run_case(name, spec, cache):
         del E
         cache.clear()
         cache[key] = defl
-    else:
+    else:  # C2(b) / C5: iterative coarse solve to rounding level (see FastDeflation.prepare)
         defl = FastDeflation(nx, ny, nz, 1.0, occ, fixed, b, op.k0)
-        defl.prepare(op)
+        defl.prepare(op, direct=False)
         cache.clear()
         cache[key] = defl
     defl.prepare = lambda *_a: None  # already prepared for this operator / topology

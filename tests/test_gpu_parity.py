@@ -370,3 +370,25 @@ def test_dpcg_c4_size_converges(tv, occ_kind):
     free = torch.from_numpy(op.free_mask).cuda()
     true_rel = float(res[free].norm() / fd[free].norm())
     assert true_rel < 1e-7, true_rel
+
+
+def test_generic_operator_path_keeps_deflation(tv, golden):
+    """solve_static with apply_op / diag (the reference's hook for shifted
+    solves, fea.py:218-299) still deflates with the space prepared for op, as
+    the reference does: with apply_op = op's own K it reproduces the default
+    device solve's iterates (same count +-1, solution 1e-10)."""
+    import torch
+
+    from paper_2203_15115_b200 import fea
+
+    d, case, fixed, f = cantilever(24, 12, 12, (24, 0, 0), (24, 12, 12))
+    occ = np.where(np.random.default_rng(3).random(d.n_elems) < 0.9, 1.0, 1e-3)
+    op = make_op(tv, (24, 12, 12), occ, fixed)
+    defl = fea.build_deflation(d, op.topology, fixed, 3)
+    fd = torch.from_numpy(f).cuda()
+    r0 = fea.solve_static(op, fd, tol=1e-10, deflation=defl, projection="reference")
+    rg = fea.solve_static(op, fd, tol=1e-10, deflation=defl, apply_op=op.apply_device)
+    rp = fea.solve_static(op, fd, tol=1e-10, apply_op=op.apply_device)
+    assert abs(rg.iterations - r0.iterations) <= 1, (rg.iterations, r0.iterations)
+    assert rel(rg.u.cpu().numpy(), r0.u.cpu().numpy()) < 1e-9
+    assert rp.iterations > rg.iterations  # without the space: plain Jacobi PCG
