@@ -68,11 +68,6 @@ static bool modal_reduce(const double* mh, Modal& m) {
 }
 
 
-__global__ void k_masked_copy(long long nn, const double* u, const uint8_t* nflags, double* out) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= 3 * nn) return;
-  out[i] = ((nflags[i / 3] >> (i % 3)) & 1) ? 0.0 : u[i];
-}
 
 // fp64 pipe probe: 8 independent DFMA chains per thread, 8 CTAs of 256 per SM
 __global__ void k_fp64_probe(double* out, int iters, double a, double b) {
@@ -232,26 +227,20 @@ int tvb_matvec(int nx, int ny, int nz, const double* h_mh45, const double* d_u, 
   const Grid g = make_grid(nx, ny, nz);
   const MatvecPlan pl = plan_matvec(g, num_sms());
   const bool mask_in = (flags & TVB_MASK_IN) != 0;
-  if ((d_dot || mask_in) && (!d_ws || ws_bytes < tvb_matvec_ws_bytes(nx, ny, nz) || pl.nblocks() > 65536)) {
+  if (d_dot && (!d_ws || ws_bytes < tvb_matvec_ws_bytes(nx, ny, nz) || pl.nblocks() > 65536)) {
     set_last_error("matvec workspace too small");
     return kStatusWorkspace;
   }
   Modal M;
   if (!modal_reduce(h_mh45, M)) return kStatusBadArg;
   cudaStream_t s = (cudaStream_t)stream;
-  const double* u = d_u;
-  if (mask_in) {
-    double* um = (double*)((char*)d_ws + matvec_partials_bytes());
-    k_masked_copy<<<(unsigned)((3 * g.nn + 255) / 256), 256, 0, s>>>(g.nn, d_u, d_nflags, um);
-    u = um;
-  }
   MatvecParams P{};
   P.g = g;
-  P.u = u;
+  P.u = d_u;
   P.y = d_out;
   P.occ = d_occ;
   P.fixed = d_nflags;
-  P.mask_in = 0;
+  P.mask_in = mask_in ? 1 : 0;  // fused into the staging (matvec.cu MASKIN)
   P.mask_out = (flags & TVB_MASK_OUT) ? 1 : 0;
   P.accumulate = (flags & TVB_ACCUMULATE) ? 1 : 0;
   P.dot_partial = d_dot ? (double*)d_ws : nullptr;
@@ -326,11 +315,6 @@ int tvb_matvec_host(int nx, int ny, int nz, const double* h_mh45, const double* 
     if (need > loaded) {
       cudaMemcpyAsync(du + pdoubles * loaded, h_u + pdoubles * loaded, sizeof(double) * pdoubles * (need - loaded),
                       cudaMemcpyHostToDevice, P.h2d);
-      if (flags & TVB_MASK_IN) {
-        const long long n0 = (long long)g.px * g.py * loaded, nn = (long long)g.px * g.py * (need - loaded);
-        k_masked_copy<<<(unsigned)((3 * nn + 255) / 256), 256, 0, P.h2d>>>(nn, du + 3 * n0, d_nflags + n0,
-                                                                             du + 3 * n0);
-      }
       loaded = need;
     }
     cudaEventRecord(P.in[k], P.h2d);
@@ -341,6 +325,7 @@ int tvb_matvec_host(int nx, int ny, int nz, const double* h_mh45, const double* 
     mp.y = dy;
     mp.occ = d_occ;
     mp.fixed = d_nflags;
+    mp.mask_in = (flags & TVB_MASK_IN) ? 1 : 0;
     mp.mask_out = (flags & TVB_MASK_OUT) ? 1 : 0;
     mp.zlo = z0;
     mp.zhi = z1;
@@ -440,11 +425,6 @@ int tvb_matvec_host_batch(int nx, int ny, int nz, const double* h_mh45, int nvec
       if (need > loaded) {
         cudaMemcpyAsync(du[b] + pdoubles * loaded, h_u[v] + pdoubles * loaded,
                         sizeof(double) * pdoubles * (need - loaded), cudaMemcpyHostToDevice, P.h2d);
-        if (flags & TVB_MASK_IN) {
-          const long long n0 = (long long)g.px * g.py * loaded, nn = (long long)g.px * g.py * (need - loaded);
-          k_masked_copy<<<(unsigned)((3 * nn + 255) / 256), 256, 0, P.h2d>>>(nn, du[b] + 3 * n0, d_nflags + n0,
-                                                                               du[b] + 3 * n0);
-        }
         loaded = need;
       }
       cudaEventRecord(P.in[k], P.h2d);
@@ -455,6 +435,7 @@ int tvb_matvec_host_batch(int nx, int ny, int nz, const double* h_mh45, int nvec
       mp.y = dy[b];
       mp.occ = d_occ;
       mp.fixed = d_nflags;
+      mp.mask_in = (flags & TVB_MASK_IN) ? 1 : 0;
       mp.mask_out = (flags & TVB_MASK_OUT) ? 1 : 0;
       mp.zlo = z0;
       mp.zhi = z1;

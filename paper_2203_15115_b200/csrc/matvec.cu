@@ -122,7 +122,11 @@ constexpr int kRing = kAhead + 1;
 //   plane k through shared memory; the owner thread finishes the node.
 // WX, WY > 0: the tile shape as compile-time constants (every index and
 // shared-memory offset of the hot loop becomes an immediate); 0: runtime shape.
-template <int NT, int MINB, bool DOT, bool MASKOUT, int WX = 0, int WY = 0>
+// MASKIN: zero the fixed DOFs of u as it is staged (the public API's
+// TVB_MASK_IN, fea.py:55-57): each thread loads the fixed-axis flags of the
+// doubles it stages with the copy and clears them in shared memory once they
+// have landed, before the step barrier -- no separate masked copy of u.
+template <int NT, int MINB, bool DOT, bool MASKOUT, int WX = 0, int WY = 0, bool MASKIN = false>
 __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
   pdl_entry();
   extern __shared__ double smem[];
@@ -223,6 +227,8 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
       }
     }
     const unsigned up_s = (unsigned)__cvta_generic_to_shared(Up), oc_s = (unsigned)__cvta_generic_to_shared(Oc);
+    // MASKIN: per ring slot, bit q = "list entry q of this thread is a fixed DOF"
+    unsigned mring = 0u;
 
     // stage node plane k and occupancy layer k into ring slot sl (zero-filled outside the grid)
     auto load_layer = [&](int k, int sl) {
@@ -237,11 +243,23 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
 #pragma unroll
         for (int q = 0; q < kStage; ++q)
           if (q < ncnt) cp_async8_s(base + (unsigned)e[q].x, src + e[q].y);
+        if (MASKIN) {
+          const uint8_t* fl = P.fixed + (long long)G.px * G.py * k;
+          unsigned bits = 0u;
+#pragma unroll
+          for (int q = 0; q < kStage; ++q)
+            if (q < ncnt) {
+              const int gd = e[q].y / 8;  // in-plane double: node gd / 3, axis gd % 3
+              bits |= ((unsigned)(fl[gd / 3] >> (gd % 3)) & 1u) << q;
+            }
+          mring = (mring & ~(15u << (4 * sl))) | (bits << (4 * sl));
+        }
       } else {  // halo plane above / below the grid (first / last piece only)
         double* dst = Up + sl * PS;
 #pragma unroll
         for (int q = 0; q < kStage; ++q)
           if (q < ncnt) dst[st_list[q * NT + t].x / 8] = 0.0;
+        if (MASKIN) mring &= ~(15u << (4 * sl));
       }
       if (has_occ) {
         if (k >= 0 && k < G.nz) cp_async8_s(oc_s + (unsigned)(8 * sl * OS) + ooff, P.occ + layer_stride * k + oeoff);
@@ -257,6 +275,17 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
       for (int b = 0; b < 4; ++b)
   #pragma unroll
         for (int a = 0; a < 3; ++a) f[3 * b + a] = pl[(b >> 1) * S + 3 * (b & 1) + a];
+    };
+
+    // MASKIN: clear this thread's fixed staged doubles of ring slot sl (after they landed)
+    auto apply_mask = [&](int sl) {
+      if (!MASKIN) return;
+      const unsigned bits = (mring >> (4 * sl)) & 15u;
+      if (bits == 0u) return;
+      double* dst = Up + sl * PS;
+#pragma unroll
+      for (int q = 0; q < kStage; ++q)
+        if ((bits >> q) & 1u) dst[st_list[q * NT + t].x / 8] = 0.0;
     };
 
     double carry[12];
@@ -314,6 +343,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
         for (int a = 0; a < 3; ++a) uo[a] = Up[sk * PS + j00 + S + 3 + a];
       }
       cp_async_wait_group<kAhead - 2>();  // plane k+2 (and occupancy k+2) landed
+      if (MASKIN && k + 2 <= kz1) apply_mask(sk == kRing - 2 ? 0 : (sk == kRing - 1 ? 1 : sk + 2));
       if (!(TVB_MV_DBG(P) & 1)) __syncthreads();
       if (out) {
         // node (x0+tx, y0+ty) = local (1,1) of this column, (0,1) of column
@@ -355,6 +385,10 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
       else cp_async_commit();
     }
     cp_async_wait_group<kAhead - 2>();
+    if (MASKIN) {  // planes kz0 - 1 and kz0 landed
+      apply_mask(s0);
+      apply_mask(s0 == kRing - 1 ? 0 : s0 + 1);
+    }
     __syncthreads();
     double fa[12], fb[12];
     gather_face(s0, fa);
@@ -428,6 +462,12 @@ MatvecPlan plan_matvec(const Grid& g, int num_sms) {
 
 template <int NT, int MINB, int WX = 0, int WY = 0>
 static void set_smem_attr(size_t bytes) {
+  if (WX == 0) {
+    cudaFuncSetAttribute(k_matvec<NT, MINB, false, false, 0, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(k_matvec<NT, MINB, false, true, 0, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(k_matvec<NT, MINB, true, false, 0, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(k_matvec<NT, MINB, true, true, 0, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  }
   cudaFuncSetAttribute(k_matvec<NT, MINB, false, false, WX, WY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   cudaFuncSetAttribute(k_matvec<NT, MINB, false, true, WX, WY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   cudaFuncSetAttribute(k_matvec<NT, MINB, true, false, WX, WY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -437,6 +477,13 @@ static void set_smem_attr(size_t bytes) {
 template <int NT, int MINB, int WX = 0, int WY = 0>
 static void launch_nt(dim3 grid, size_t smem, cudaStream_t s, const MatvecParams& P, const Modal& M) {
   const bool dot = P.dot_partial != nullptr, mo = P.mask_out && P.fixed != nullptr;
+  if (P.mask_in && P.fixed != nullptr) {  // fused input mask: runtime-shape kernel
+    if (dot && mo) launch_k(k_matvec<NT, MINB, true, true, 0, 0, true>, grid, NT, smem, s, P, M);
+    else if (dot) launch_k(k_matvec<NT, MINB, true, false, 0, 0, true>, grid, NT, smem, s, P, M);
+    else if (mo) launch_k(k_matvec<NT, MINB, false, true, 0, 0, true>, grid, NT, smem, s, P, M);
+    else launch_k(k_matvec<NT, MINB, false, false, 0, 0, true>, grid, NT, smem, s, P, M);
+    return;
+  }
   if (dot && mo) launch_k(k_matvec<NT, MINB, true, true, WX, WY>, grid, NT, smem, s, P, M);
   else if (dot) launch_k(k_matvec<NT, MINB, true, false, WX, WY>, grid, NT, smem, s, P, M);
   else if (mo) launch_k(k_matvec<NT, MINB, false, true, WX, WY>, grid, NT, smem, s, P, M);
@@ -447,7 +494,7 @@ static void launch_nt(dim3 grid, size_t smem, cudaStream_t s, const MatvecParams
 // BASELINE grids (C2 23x11, C4 25x10, C5 28x9, C1 / C3 42x6)
 static bool launch_fixed_shape(const MatvecPlan& pl, dim3 grid, cudaStream_t s, const MatvecParams& P, const Modal& M) {
   static const bool off = getenv("TVB_MV_GENERIC") != nullptr;
-  if (off || pl.nt != 256) return false;
+  if (off || pl.nt != 256 || (P.mask_in && P.fixed != nullptr)) return false;
 #define TVB_SHAPE(X, Y)                                  \
   if (pl.wx == X && pl.wy == Y) {                        \
     launch_nt<256, 2, X, Y>(grid, pl.smem, s, P, M);     \
