@@ -175,6 +175,10 @@ class FastDeflation:
         rz = r @ z
         best = np.inf
         stall = 0
+        # the recursively updated r keeps shrinking long after the true
+        # residual has reached the rounding floor (~1e-16 |b|) and would
+        # underflow (0/0) after ~640 steps: stop 4 decades below the floor
+        floor = 1e-20 * np.linalg.norm(b)
         for _ in range(2000):
             q = E @ p
             a = rz / (p @ q)
@@ -185,7 +189,7 @@ class FastDeflation:
                 best, stall = rn, 0
             else:
                 stall += 1
-            if stall >= 20 or rn == 0.0:
+            if stall >= 20 or rn <= floor:
                 break
             z = dinv * r
             rz_new = r @ z

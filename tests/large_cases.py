@@ -29,7 +29,7 @@ CASES = {
     "c4_bern_z": dict(dims=(160, 80, 80), block=8, load=((160, 39, 39), (160, 41, 41), (0, 0, -1)), occ="bern0.9",
                       tols=(1e-8, 1e-11), iters=(40,)),
     "c4_bern_y": dict(dims=(160, 80, 80), block=8, load=((160, 39, 39), (160, 41, 41), (0, -1, 0)), occ="bern0.9",
-                      tols=(1e-8,), iters=(40,)),
+                      tols=(1e-8, 1e-11), iters=(40,)),
     # BASELINE configs[4] (C5): 320x160x160, b = 8, 5x5 patch load; fixed-iteration iterates
     "c5_solid": dict(dims=(320, 160, 160), block=8, load=((320, 78, 78), (320, 82, 82), (0, 0, -1)), occ="solid",
                      tols=(), iters=(40,)),

@@ -5,13 +5,23 @@ the reference's operator, deflation space and loop; a sparse exact coarse
 solve instead of the dense cho_solve).
 
 Per recorded stop of the reference (tolerance 1e-8 / 1e-11, or a fixed
-iteration count k):
-  * tolerance stops: the device solve at that tolerance stops within +-1
+iteration count k), following SURVEY §0.5 / §8(c) ("parity of the solution
+must be judged at a tight tolerance or at a fixed iteration count; report
+tol 1e-8 differences alongside, as information" -- the reference's own two
+backends are 1.2e-10 apart at a 1e-8 stop):
+  * every tolerance stop: the device solve at that tolerance stops within +-1
     iteration of the reference, and its compliance f.u matches to 1e-8;
-  * every recorded iterate: the device iterate after the SAME number of
-    iterations (solve_static with that max_iters; NoConvergence carries the
-    iterate) matches the reference's within 1e-10 relative (north-star
-    solution tolerance) at 4096 seeded sample DOFs, in norm and in f.u.
+  * tight stops (1e-11) and fixed-iteration iterates: the device iterate after
+    the SAME number of iterations (solve_static with that max_iters;
+    NoConvergence carries the iterate) matches the reference's within 1e-10
+    relative (north-star solution tolerance) at 4096 seeded sample DOFs, in
+    norm and in f.u;
+  * 1e-8 stops: the same comparison is reported, and bounded by 1e-9 (the
+    order of the iterate's own truncation error, 3e-10 .. 1.4e-9 on these
+    problems). Measured: <= 2.5e-11 except the two C4 Bernoulli(0.9) cases
+    after ~940 iterations (7.5e-11 and 1.2e-10; the reference against itself
+    with K.u rounded differently moves 8.5e-12 there, tests/golden/
+    noise_floor.py).
 
 (The reference's recurrence diverges at 1e-12 on some of these problems --
 e.g. the C1 geometry with a face load reaches residual 8.8e3 at its iteration
@@ -27,6 +37,7 @@ import large_cases as LC
 
 FIX = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "large_dpcg.npz")
 SOL_TOL = 1e-10   # north star: PCG solution within 1e-10 relative
+LOOSE_TOL = 1e-9  # iterate at a 1e-8 stop (information): order of its truncation error
 J_TOL = 1e-8      # north star: compliance within 1e-8 relative
 
 
@@ -111,6 +122,7 @@ def test_dpcg_matches_reference_at_full_size(name):
         e_u = _rel(xs, u_ref)
         e_n = abs(float(x.norm()) - float(fx[f"{name}_{tag}_norm"])) / float(fx[f"{name}_{tag}_norm"])
         e_j = abs(float(fd @ x) - J_ref) / abs(J_ref)
+        bound = LOOSE_TOL if tag == "tol1e-08" else SOL_TOL
         report.append(f"x_{it_ref}: u rel {e_u:.1e} |u| rel {e_n:.1e} J rel {e_j:.1e}")
-        assert e_u <= SOL_TOL and e_n <= SOL_TOL and e_j <= SOL_TOL, (name, tag, e_u, e_n, e_j)
+        assert e_u <= bound and e_n <= bound and e_j <= bound, (name, tag, e_u, e_n, e_j, bound)
     print(f"[large parity] {name}: " + "; ".join(report))
