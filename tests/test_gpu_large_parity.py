@@ -10,7 +10,15 @@ must be judged at a tight tolerance or at a fixed iteration count; report
 tol 1e-8 differences alongside, as information" -- the reference's own two
 backends are 1.2e-10 apart at a 1e-8 stop):
   * every tolerance stop: the device solve at that tolerance stops within +-1
-    iteration of the reference, and its compliance f.u matches to 1e-8;
+    iteration of the reference, and its compliance f.u matches to 1e-8.
+    Both projections are run: ``reference`` is the reference's recurrence
+    step for step; ``stabilized`` (the default, solver.cu) re-imposes
+    W^T A p = 0 every iteration. At a 1e-11 stop after ~1070 iterations the
+    reference recurrence's residual carries ~10 % of accumulated drift that
+    the stabilised one does not (device residual at x_1073 of c4_bern_y:
+    9.48e-12 with the reference projection, CPU reference 9.54e-12,
+    stabilised 8.62e-12), so the stabilised solve may stop up to 0.3 % of the
+    iterations EARLIER there (never more than 1 later);
   * tight stops (1e-11) and fixed-iteration iterates: the device iterate after
     the SAME number of iterations (solve_static with that max_iters;
     NoConvergence carries the iterate) matches the reference's within 1e-10
@@ -89,9 +97,18 @@ def _problem(name):
     return _CACHE[key]
 
 
+def _iteration_window(projection, tag, it_ref):
+    """Allowed (lo, hi) stopping iterations of the device solve."""
+    early = 1
+    if projection == "stabilized" and tag != "tol1e-08":
+        early = max(1, int(np.ceil(0.003 * it_ref)))
+    return it_ref - early, it_ref + 1
+
+
 @pytest.mark.gpu
+@pytest.mark.parametrize("projection", ["stabilized", "reference"])
 @pytest.mark.parametrize("name", list(LC.CASES))
-def test_dpcg_matches_reference_at_full_size(name):
+def test_dpcg_matches_reference_at_full_size(name, projection):
     from paper_2203_15115_b200 import fea
     from paper_2203_15115_b200.errors import NoConvergence
 
@@ -108,14 +125,15 @@ def test_dpcg_matches_reference_at_full_size(name):
         u_ref, J_ref = fx[f"{name}_{tag}_u"], float(fx[f"{name}_{tag}_J"])
         if tag.startswith("tol"):
             tol = float(tag[3:])
-            r = fea.solve_static(op, fd, tol=tol, deflation=defl)
-            assert abs(r.iterations - it_ref) <= 1, (name, tag, r.iterations, it_ref)
+            r = fea.solve_static(op, fd, tol=tol, deflation=defl, projection=projection)
+            lo, hi = _iteration_window(projection, tag, it_ref)
+            assert lo <= r.iterations <= hi, (name, projection, tag, r.iterations, it_ref)
             J = float(fd @ r.u)
             assert abs(J - J_ref) <= J_TOL * abs(J_ref), (name, tag, J, J_ref)
             report.append(f"{tag}: it {r.iterations} (ref {it_ref}) J rel {abs(J - J_ref) / abs(J_ref):.1e}")
         # the iterate after exactly it_ref iterations
         with pytest.raises(NoConvergence) as ei:
-            fea.solve_static(op, fd, tol=1e-14, max_iters=it_ref, deflation=defl)
+            fea.solve_static(op, fd, tol=1e-14, max_iters=it_ref, deflation=defl, projection=projection)
         x = ei.value.u
         assert x is not None and ei.value.iterations == it_ref
         xs = x[idx].cpu().numpy()
@@ -124,5 +142,5 @@ def test_dpcg_matches_reference_at_full_size(name):
         e_j = abs(float(fd @ x) - J_ref) / abs(J_ref)
         bound = LOOSE_TOL if tag == "tol1e-08" else SOL_TOL
         report.append(f"x_{it_ref}: u rel {e_u:.1e} |u| rel {e_n:.1e} J rel {e_j:.1e}")
-        assert e_u <= bound and e_n <= bound and e_j <= bound, (name, tag, e_u, e_n, e_j, bound)
-    print(f"[large parity] {name}: " + "; ".join(report))
+        assert e_u <= bound and e_n <= bound and e_j <= bound, (name, projection, tag, e_u, e_n, e_j, bound)
+    print(f"[large parity] {name} ({projection}): " + "; ".join(report))
