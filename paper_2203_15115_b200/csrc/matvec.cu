@@ -158,8 +158,16 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
   // tile-major; CTA b takes the contiguous range [w0, w1) and walks it as
   // (tile, plane range) pieces.
   const int zlo = P.zlo, zhi = P.zhi < 0 ? G.pz : P.zhi, npl = zhi - zlo;  // output node planes
-  const long long W = (long long)P.ntiles * npl;
-  const long long w0 = W * blockIdx.x / gridDim.x, w1 = W * (blockIdx.x + 1) / gridDim.x;
+  // Every piece pays a fixed overhead (its halo layer and the fill of the
+  // staging pipeline, ~piece_cost plane-steps), and a range that crosses a
+  // tile boundary pays it twice: split a virtual length in which each tile is
+  // preceded by piece_cost overhead units, so such CTAs get fewer planes.
+  const long long VT = npl + P.piece_cost, V = (long long)P.ntiles * VT;
+  auto to_work = [&](long long v) {
+    const long long tl = v / VT, r = v - tl * VT;
+    return tl * npl + (r > P.piece_cost ? r - P.piece_cost : 0);
+  };
+  const long long w0 = to_work(V * blockIdx.x / gridDim.x), w1 = to_work(V * (blockIdx.x + 1) / gridDim.x);
   for (long long w = w0; w < w1;) {
     const int tile = (int)(w / npl);
     const int kz0 = zlo + (int)(w % npl);
@@ -514,6 +522,10 @@ cudaError_t launch_matvec(const MatvecPlan& pl, MatvecParams P, const Modal& M, 
   P.ntx = pl.ntx;
   P.ntiles = pl.ntx * pl.nty;
   if (const char* d = getenv("TVB_MV_DEBUG")) P.debug = atoi(d);
+  // measured (scripts/gpu_piece_cost.sh, same box): charge 3 vs 0 -> C2(a) K.u 53.0 -> 51.0 us (warm),
+  // C4 DPCG 215.0 -> 212.0, C3 117.3 -> 114.1 us per iteration; 2 / 4 / 6 within 0.5 us of 3
+  static const int piece_cost = getenv("TVB_MV_PIECE_COST") ? atoi(getenv("TVB_MV_PIECE_COST")) : 3;
+  P.piece_cost = piece_cost < 0 ? 0 : piece_cost;
   static bool attr_set = false;
   if (!attr_set) {
     set_smem_attr<256, 2>(110 * 1024);

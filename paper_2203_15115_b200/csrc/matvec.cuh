@@ -19,6 +19,7 @@ struct MatvecParams {
   double* dot_partial;    // per-CTA partial of sum(u_owned * y_owned), or nullptr
   const int* stop;        // if non-null and *stop != 0 the launch is a no-op (solver done)
   int zlo = 0, zhi = -1;  // output node planes [zlo, zhi) (zhi < 0: all); reads input planes [zlo-1, zhi]
+  int piece_cost = 0;     // per-piece overhead in plane-steps (halo layer + pipeline fill) charged by the work split
 };
 
 // nt threads per CTA, wx x wy element-column tiles (ntx x nty of them),
