@@ -82,6 +82,104 @@ cudaError_t launch_dense_gemv_multi(long long nc, const double* Einv, int ncols,
   return cudaGetLastError();
 }
 
+// Dense coarse solve and nu_B = S_B mu_B in one launch (the iteration's dense
+// path). One CTA per agglomerate, kNuWpr warps per coarse row: with one warp
+// per row a C1-sized system (1500 rows) puts only ~10 warps on an SM and the
+// 18 MB inverse streams at L2 latency (ncu 10.7 us); four warps per row, each
+// summing a contiguous quarter of the row lane-strided with four loads in
+// flight, then combined in segment order, keep ~40 warps per SM busy. The six
+// mu values go through shared memory and threads 0..5 (per column) apply S_B
+// in k_block_nu's order. Deterministic (fixed orders); per column the
+// arithmetic does not depend on MC, so batched and single solves stay bitwise
+// equal.
+constexpr int kNuWpr = 4;
+
+template <int MC>
+__global__ void __launch_bounds__(6 * kNuWpr * 32) k_dense_gemv_nu(long long nb, const double* __restrict__ Einv,
+                                                                   const double* __restrict__ S,
+                                                                   const double* __restrict__ yc, long long ldy,
+                                                                   double* mu, long long ldm, double* nu,
+                                                                   long long ldn, const int* stop,
+                                                                   long long stop_ld) {
+  pdl_entry();
+  __shared__ double part[MC][6][kNuWpr];
+  __shared__ double mu_s[MC][6];
+  if (stop != nullptr) {
+    bool all = true;
+#pragma unroll
+    for (int c = 0; c < MC; ++c) all = all && stop[c * stop_ld] != 0;
+    if (all) return;
+  }
+  const long long B = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = warp / kNuWpr, q = warp % kNuWpr;  // row of the block, segment of the row
+  const long long nc = 6 * nb, row = 6 * B + r;
+  const long long seg = ((nc + kNuWpr - 1) / kNuWpr + 31) & ~31LL;  // segment length, a multiple of 32
+  const long long j0 = q * seg, j1 = min(nc, j0 + seg);
+  const double* a = Einv + row * nc;
+  double acc[MC];
+#pragma unroll
+  for (int c = 0; c < MC; ++c) acc[c] = 0.0;
+  long long j = j0 + lane;
+  for (; j + 96 < j1; j += 128) {  // four independent row loads in flight, accumulated in index order
+    const double a0 = a[j], a1 = a[j + 32], a2 = a[j + 64], a3 = a[j + 96];
+#pragma unroll
+    for (int c = 0; c < MC; ++c) {
+      const double* y = yc + c * ldy + j;
+      acc[c] = fma(a0, y[0], acc[c]);
+      acc[c] = fma(a1, y[32], acc[c]);
+      acc[c] = fma(a2, y[64], acc[c]);
+      acc[c] = fma(a3, y[96], acc[c]);
+    }
+  }
+  for (; j < j1; j += 32) {
+    const double aj = a[j];
+#pragma unroll
+    for (int c = 0; c < MC; ++c) acc[c] = fma(aj, yc[c * ldy + j], acc[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < MC; ++c) {
+    const double v = warp_sum(acc[c]);
+    if (lane == 0) part[c][r][q] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 6 * MC) {
+    const int c = threadIdx.x / 6, i = threadIdx.x % 6;
+    double v = part[c][i][0];
+#pragma unroll
+    for (int k = 1; k < kNuWpr; ++k) v += part[c][i][k];
+    mu[c * ldm + 6 * B + i] = v;
+    mu_s[c][i] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 6 * MC) {
+    const int c = threadIdx.x / 6, i = threadIdx.x % 6;
+    double v = 0.0;
+    for (int k = 0; k < 6; ++k) v = fma(S[36 * B + i + 6 * k], mu_s[c][k], v);
+    nu[c * ldn + 6 * B + i] = v;
+  }
+}
+
+cudaError_t launch_dense_gemv_nu_multi(long long nb, const double* Einv, const double* S, int ncols, const double* yc,
+                                       long long ldy, double* mu, long long ldm, double* nu, long long ldn,
+                                       const int* stop, long long stop_ld, cudaStream_t s) {
+  for (int c0 = 0; c0 < ncols; c0 += 4) {
+    const int k = ncols - c0 < 4 ? ncols - c0 : 4;
+    const double* y = yc + c0 * ldy;
+    double* m = mu + c0 * ldm;
+    double* n = nu + c0 * ldn;
+    const int* st = stop ? stop + c0 * stop_ld : nullptr;
+    const unsigned grid = (unsigned)nb;
+    switch (k) {
+      case 1: launch_k(k_dense_gemv_nu<1>, grid, 6 * kNuWpr * 32, 0, s, nb, Einv, S, y, ldy, m, ldm, n, ldn, st, stop_ld); break;
+      case 2: launch_k(k_dense_gemv_nu<2>, grid, 6 * kNuWpr * 32, 0, s, nb, Einv, S, y, ldy, m, ldm, n, ldn, st, stop_ld); break;
+      case 3: launch_k(k_dense_gemv_nu<3>, grid, 6 * kNuWpr * 32, 0, s, nb, Einv, S, y, ldy, m, ldm, n, ldn, st, stop_ld); break;
+      default: launch_k(k_dense_gemv_nu<4>, grid, 6 * kNuWpr * 32, 0, s, nb, Einv, S, y, ldy, m, ldm, n, ldn, st, stop_ld); break;
+    }
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dense_gemv(long long nc, const double* Einv, const double* yc, double* mu, const int* stop,
                               cudaStream_t s) {
   return launch_dense_gemv_multi(nc, Einv, 1, yc, 0, mu, 0, stop, 0, s);
@@ -430,12 +528,21 @@ int pcg_solve_multi(const PcgProblem& P, PcgResult* R, int* rstat, cudaStream_t 
     }
     if (!defl) return cudaSuccess;
     if ((e = join_to_s()) != cudaSuccess) return e;
-    if (!(skip & 16) && (e = coarse_solve(c_lo, c_hi - c_lo, &W[c_lo].st->done)) != cudaSuccess) return e;
+    // dense coarse inverse: mu and nu = S mu in one launch (k_dense_gemv_nu); TVB_DENSE_NU_FUSED=0: two launches
+    static const bool fuse_nu_env = !(getenv("TVB_DENSE_NU_FUSED") && atoi(getenv("TVB_DENSE_NU_FUSED")) == 0);
+    const bool fused_nu = fuse_nu_env && P.coarse_kind != 1 && !(skip & 48);
+    if (fused_nu) {
+      if ((e = launch_dense_gemv_nu_multi(A.nb, P.coarse, P.S, c_hi - c_lo, W[c_lo].yc, ldc, W[c_lo].mu, ldc,
+                                          W[c_lo].nu, ldc, &W[c_lo].st->done, ld_done, s)) != cudaSuccess)
+        return e;
+    } else if (!(skip & 16) && (e = coarse_solve(c_lo, c_hi - c_lo, &W[c_lo].st->done)) != cudaSuccess) {
+      return e;
+    }
     if ((e = fork_from_s()) != cudaSuccess) return e;
     if (skip & 32) return cudaSuccess;
     for (int c = c_lo; c < c_hi; ++c) {
       const int* stop = &W[c].st->done;
-      if ((e = launch_block_nu(A, D, W[c].mu, W[c].nu, sc(c), stop)) != cudaSuccess) return e;
+      if (!fused_nu && (e = launch_block_nu(A, D, W[c].mu, W[c].nu, sc(c), stop)) != cudaSuccess) return e;
       // p = z + beta p - W nu, and the deferred x += alpha p_old of this iteration
       if ((e = launch_prolong(A, P.dflags, D, W[c].nu, W[c].p, W[c].z, W[c].st, 1, sc(c), P.xs[c])) != cudaSuccess)
         return e;
