@@ -396,12 +396,14 @@ __global__ void __launch_bounds__(kRestrictWarpThreads) k_restrict_warp(Agglo A,
 cudaError_t launch_restrict(const Agglo& A, const uint8_t* nflags, DeflData D, const double* y, double* yc,
                             cudaStream_t s, const int* stop, const double* y2, const void* state) {
   const SolverState* st = (const SolverState*)state;
-  static int mode = -1;  // TVB_RESTRICT=cta|warp (A/B); default: warp per block below 8^3 blocks
+  static int mode = -1;  // TVB_RESTRICT=cta|warp (A/B); default: warp per block below 8^3 blocks when there are > 1000
   if (mode < 0) {
     const char* e = getenv("TVB_RESTRICT");
     mode = e == nullptr ? 0 : (e[0] == 'w' ? 1 : 2);
   }
-  const bool warp = mode == 1 || (mode == 0 && A.b < 8);
+  // few small blocks (C1: 250): one CTA per block spreads them over the SMs (C1 solve 5.29 -> 5.11 ms);
+  // at C3's 2000 blocks the warp-per-block kernel is ahead again (113.4 vs 115.2 us per iteration)
+  const bool warp = mode == 1 || (mode == 0 && A.b < 8 && A.nb > 1000);
   if (warp) {
     const unsigned gw = (unsigned)((A.nb + 7) / 8);
     if (A.b == 8) launch_k(k_restrict_warp<8>, gw, kRestrictWarpThreads, 0, s, A, nflags, D, y, y2, st, yc, stop);
