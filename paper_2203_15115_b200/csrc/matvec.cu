@@ -445,25 +445,49 @@ MatvecPlan plan_matvec(const Grid& g, int num_sms) {
   }
   MatvecPlan best{};
   double best_cost = 1e300;
+  auto plan_cost = [&](int nt, int wx, int wy, MatvecPlan& out) {
+    const int nc = num_sms * ctas_per_sm(nt);
+    const int ntx = (g.px + wx - 2) / (wx - 1);
+    const int nty = (g.py + wy - 2) / (wy - 1);
+    const double tiles = (double)ntx * nty;
+    const int warps = nt / 32;
+    const double pieces = std::max(tiles, (double)nc) + nc;  // upper bound of pieces
+    out = MatvecPlan{nt, wx, wy, ntx, nty, nc, matvec_smem(nt, wx, wy)};
+    return (tiles * g.pz + 1.5 * pieces) * warps / nc;
+  };
   // wx < 20 loses to short staged rows and frequent warp row-wraps (measured
   // sweeps, profiles/README.md); nt = 384 / 512 never won.
   for (int nt : {256, 384}) {
-    const int nc = num_sms * ctas_per_sm(nt);
     for (int wx = 20; wx <= 48; ++wx) {
       for (int wy = 3; wx * wy <= nt; ++wy) {
         if (wx * wy < nt - 48) continue;
-        const int ntx = (g.px + wx - 2) / (wx - 1);
-        const int nty = (g.py + wy - 2) / (wy - 1);
-        const double tiles = (double)ntx * nty;
-        const int warps = nt / 32;
-        const double pieces = std::max(tiles, (double)nc) + nc;  // upper bound of pieces
-        const double cost = (tiles * g.pz + 1.5 * pieces) * warps / nc;
+        MatvecPlan pl;
+        const double cost = plan_cost(nt, wx, wy, pl);
         if (cost < best_cost - 1e-9 || (cost <= best_cost + 1e-9 && wx > best.wx)) {
           best_cost = cost;
-          best = MatvecPlan{nt, wx, wy, ntx, nty, nc, matvec_smem(nt, wx, wy)};
+          best = pl;
         }
       }
     }
+  }
+  // The tile shapes compiled with constant geometry (launch_fixed_shape) run
+  // ~1.45x faster than the runtime-shape kernel at equal tiling (C4: 25x10
+  // 34.9 us, 24x10 51.2 us; 100^3: 47.3 vs 53.1 us; profiles/README.md), so a
+  // grid whose best generic tiling is not one of them still takes the best
+  // compiled shape unless the generic tiling is predicted to save more.
+  if (getenv("TVB_MV_GENERIC") == nullptr) {
+    static const int fixed_shapes[4][2] = {{23, 11}, {25, 10}, {28, 9}, {42, 6}};
+    MatvecPlan fbest{};
+    double fcost = 1e300;
+    for (const auto& sh : fixed_shapes) {
+      MatvecPlan pl;
+      const double cost = plan_cost(256, sh[0], sh[1], pl);
+      if (cost < fcost) {
+        fcost = cost;
+        fbest = pl;
+      }
+    }
+    if (fcost <= 1.4 * best_cost) return fbest;
   }
   return best;
 }
