@@ -194,6 +194,12 @@ __global__ void k_loop_cond(cudaGraphConditionalHandle h, const int* done, long 
   cudaGraphSetConditional(h, go);
 }
 
+// count the nodes with an operator-fixed axis that the deflation space's flags do not fix
+__global__ void k_flags_uncovered(long long nn, const uint8_t* nflags, const uint8_t* dflags, int* count) {
+  const long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (n < nn && ((nflags[n] & 7) & ~(dflags[n] & 7))) atomicAdd(count, 1);
+}
+
 // ---------------------------------------------------------------------------
 struct PcgWork {
   double *r, *z, *p, *q, *t, *inv_d;
@@ -365,6 +371,24 @@ int pcg_solve_multi(const PcgProblem& P, PcgResult* R, int* rstat, cudaStream_t 
   TVB_CK(launch_inv_diag(G, P.occ, P.nflags, P.kdiag, W[0].inv_d, nullptr, W[0].zero_free, s));
   int zero_free = 0;
   TVB_CK(cudaMemcpyAsync(&zero_free, W[0].zero_free, sizeof(int), cudaMemcpyDeviceToHost, s));
+  // The iteration's matvecs skip the output mask (q and A z then hold
+  // arbitrary values on fixed DOFs): the update kernel keeps r = z = 0 there
+  // (inv_d == 0), p is 0 there so p.q is unaffected, and the restriction masks
+  // the fixed DOFs of ITS flags -- valid when those cover the operator's
+  // (always, unless the deflation space was built for another Dirichlet set:
+  // then the masks stay on). TVB_SOLVE_MASKOUT=1 keeps them (A/B; bitwise
+  // identical results either way).
+  bool iter_mask_out = getenv("TVB_SOLVE_MASKOUT") && atoi(getenv("TVB_SOLVE_MASKOUT")) != 0;
+  if (!iter_mask_out && defl && P.dflags != P.nflags) {
+    int* d_unc = W[0].zero_free;  // reused after its read-back below
+    TVB_CK(cudaStreamSynchronize(s));
+    TVB_CK(cudaMemsetAsync(d_unc, 0, sizeof(int), s));
+    k_flags_uncovered<<<(unsigned)((G.nn + 255) / 256), 256, 0, s>>>(G.nn, P.nflags, P.dflags, d_unc);
+    int unc = 0;
+    TVB_CK(cudaMemcpyAsync(&unc, d_unc, sizeof(int), cudaMemcpyDeviceToHost, s));
+    TVB_CK(cudaStreamSynchronize(s));
+    iter_mask_out = unc != 0;
+  }
   bool active[kPcgMaxRhs];
   int n_active = 0;
   const int one = 1;
@@ -496,7 +520,7 @@ int pcg_solve_multi(const PcgProblem& P, PcgResult* R, int* rstat, cudaStream_t 
         mp.y = W[c].q;
         mp.occ = P.occ;
         mp.fixed = P.nflags;
-        mp.mask_out = 1;
+        mp.mask_out = iter_mask_out ? 1 : 0;
         mp.dot_partial = W[c].partials + 2 * kMaxReduceCtas;
         mp.stop = stop;
         if ((e = launch_matvec(plan, mp, P.modal, cs)) != cudaSuccess) return e;
@@ -517,7 +541,7 @@ int pcg_solve_multi(const PcgProblem& P, PcgResult* R, int* rstat, cudaStream_t 
         mp.y = W[c].t;
         mp.occ = P.occ;
         mp.fixed = P.nflags;
-        mp.mask_out = 1;
+        mp.mask_out = iter_mask_out ? 1 : 0;
         mp.stop = stop;
         if ((e = launch_matvec(plan, mp, P.modal, cs)) != cudaSuccess) return e;
       }

@@ -101,9 +101,12 @@ __global__ void k_pcg_update(long long n, double* x, double* r, double* z, const
   double rr = 0.0, rz = 0.0;
   for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     if (x != nullptr) x[i] = fma(alpha, p[i], x[i]);
-    const double ri = fma(-alpha, q[i], r[i]);
+    // inv_d == 0 marks a fixed DOF: r stays 0 there whatever q holds (the
+    // iteration's matvecs do not mask their output, see k_pcg_update_v2)
+    const double di = inv_d[i];
+    const double ri = di == 0.0 ? 0.0 : fma(-alpha, q[i], r[i]);
     r[i] = ri;
-    const double zi = inv_d[i] * ri;
+    const double zi = di * ri;
     z[i] = zi;
     rr = fma(ri, ri, rr);
     rz = fma(ri, zi, rz);
@@ -199,9 +202,13 @@ __global__ void __launch_bounds__(256) k_pcg_update_v2(long long n, double* __re
       xi.y = fma(alpha, o.p.y, xi.y);
       __stcs(x2 + k, xi);  // x and r are next read one iteration later: evict first
     }
+    // inv_d == 0 marks a fixed DOF (k_inv_diag; a zero diagonal on a free DOF
+    // aborts the solve before the loop): r stays exactly 0 there whatever q
+    // holds, so the iteration's matvecs need no output mask (3.7 us per K.u
+    // at C4) -- r, z and both sums are bitwise those of the masked form
     double2 ri = o.r;
-    ri.x = fma(-alpha, o.q.x, ri.x);
-    ri.y = fma(-alpha, o.q.y, ri.y);
+    ri.x = o.d.x == 0.0 ? 0.0 : fma(-alpha, o.q.x, ri.x);
+    ri.y = o.d.y == 0.0 ? 0.0 : fma(-alpha, o.q.y, ri.y);
     double2 zi;
     zi.x = o.d.x * ri.x;
     zi.y = o.d.y * ri.y;
@@ -226,7 +233,7 @@ __global__ void __launch_bounds__(256) k_pcg_update_v2(long long n, double* __re
   if ((n & 1) && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {  // odd tail element
     const long long k = n - 1;
     if (WX) x[k] = fma(alpha, p[k], x[k]);
-    const double rk = fma(-alpha, q[k], r[k]);
+    const double rk = inv_d[k] == 0.0 ? 0.0 : fma(-alpha, q[k], r[k]);
     r[k] = rk;
     const double zk = inv_d[k] * rk;
     z[k] = zk;

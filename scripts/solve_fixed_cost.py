@@ -21,8 +21,11 @@ f = torch.from_numpy(tv.assemble_force(d, case)).cuda()
 op = fea.StiffnessOperator(d, tv.Topology(d, np.ones(d.n_elems)), tv.Material(E=1.0, nu=0.3), fixed)
 defl = fea.build_deflation(d, op.topology, fixed, b)
 defl.prepare(op)
-fea.solve_static(op, f, tol=1e-8, deflation=defl)
-for k in (8, 16, 32, 64, 96, 100000):
+try:
+    fea.solve_static(op, f, tol=1e-8, deflation=defl, max_iters=64)
+except NoConvergence:
+    pass
+for k in (8, 16, 32, 64, 96) + (() if os.environ.get('TVB_EXP_NOMASK') else (100000,)):
     ts = []
     for _ in range(7):
         torch.cuda.synchronize()
