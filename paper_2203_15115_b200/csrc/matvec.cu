@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
   #pragma unroll
           for (int a = 0; a < 3; ++a) {
             double w = ((fx >> a) & 1) ? 0.0 : v[a];
-            if (P.accumulate) w += yrow[a];
+            if (WX == 0 && P.accumulate) w += yrow[a];  // y += A u: runtime-shape kernel only (launch_fixed_shape)
             if (!(TVB_MV_DBG(P) & 4)) yrow[a] = w;
             if (DOT) dot = fma(uo[a], w, dot);
           }
@@ -526,7 +526,7 @@ static void launch_nt(dim3 grid, size_t smem, cudaStream_t s, const MatvecParams
 // BASELINE grids (C2 23x11, C4 25x10, C5 28x9, C1 / C3 42x6)
 static bool launch_fixed_shape(const MatvecPlan& pl, dim3 grid, cudaStream_t s, const MatvecParams& P, const Modal& M) {
   static const bool off = getenv("TVB_MV_GENERIC") != nullptr;
-  if (off || pl.nt != 256 || (P.mask_in && P.fixed != nullptr)) return false;
+  if (off || pl.nt != 256 || (P.mask_in && P.fixed != nullptr) || P.accumulate) return false;
 #define TVB_SHAPE(X, Y)                                  \
   if (pl.wx == X && pl.wy == Y) {                        \
     launch_nt<256, 2, X, Y>(grid, pl.smem, s, P, M);     \
