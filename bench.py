@@ -332,7 +332,7 @@ def main():
         "value_median": nd / (step_stats["median_ms"] / 1e3) / 1e9 * world,
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": ncu_traffic("k_matvec_c2_r02c", "k_matvec_c2_r02b", "k_matvec_c2_r02", "k_matvec_c2_r01c", "k_matvec_c2_r01b", "k_matvec_c2"),
+            "traffic": ncu_traffic("k_matvec_c2_r02d", "k_matvec_c2_r02c", "k_matvec_c2_r02b", "k_matvec_c2_r02", "k_matvec_c2_r01c", "k_matvec_c2_r01b", "k_matvec_c2"),
             "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes,
             "own_bound": {"t_hbm_us": t_hbm * 1e6, "t_fp64_issue_us": t_fp64 * 1e6,
                           "fp64_ops_per_elem": MATVEC_FP64_OPS, "p64_tflops_live": p64,
