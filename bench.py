@@ -396,9 +396,18 @@ def dpcg_roofline(d, defl, us_per_iter, p64, hbm):
     w = 6 * (m[0] * m[1] + m[0] + 1)
     t_r = max(1152.0 * d.n_elems / (p64 * 1e12), 8.0 * (d.n_dofs + d.n_elems) / (hbm * 1e9))
     t_survey = t_mv + t_r + 88.0 * d.n_dofs / (hbm * 1e9) + 16.0 * 6 * defl.n_blocks * w / (hbm * 1e9)
+    # Executed-algorithm bound: the matvec at the bound of the kernel
+    # that actually runs -- max(its bytes / HBM, its ~158 fp64 operations per
+    # element at the fp64 pipe's lane rate) -- instead of the dense-k0 flops;
+    # the other stages as above.
+    t_mv_own = max(8.0 * (2 * d.n_dofs + d.n_elems) / (hbm * 1e9),
+                   MATVEC_FP64_OPS * d.n_elems / (0.5 * p64 * 1e12))
+    t_exec = t_star - 2 * t_mv + 2 * t_mv_own
     return {"t_star_us": t_star * 1e6, "frac": t_star * 1e6 / us_per_iter,
             "stages_us": {k: round(v * 1e6, 2) for k, v in stages.items()},
             "survey_def": {"t_star_us": t_survey * 1e6, "frac": t_survey * 1e6 / us_per_iter},
+            "executed_def": {"t_star_us": t_exec * 1e6, "frac": t_exec * 1e6 / us_per_iter,
+                             "matvec_own_bound_us": round(t_mv_own * 1e6, 2)},
             "p64_tflops": p64, "hbm_gbs": hbm}
 
 
