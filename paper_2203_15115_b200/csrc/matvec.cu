@@ -216,7 +216,9 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
         const int i = t + q * NT;
         if (i < nval) {
           const int jy = jy_lo + i / rw, r = r_lo + i % rw;
-          st_list[q * NT + t] = make_int2(8 * (jy * S + r), 8 * (3 * G.px * (y0 - 1 + jy) + 3 * (x0 - 1) + r));
+          // MASKIN: the staged double's axis (r = 3 * node + axis) rides in the low bits of the smem byte offset
+          st_list[q * NT + t] = make_int2(8 * (jy * S + r) | (MASKIN ? r % 3 : 0),
+                                          8 * (3 * G.px * (y0 - 1 + jy) + 3 * (x0 - 1) + r));
           ncnt = q + 1;
         }
       }
@@ -235,11 +237,16 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
       }
     }
     const unsigned up_s = (unsigned)__cvta_generic_to_shared(Up), oc_s = (unsigned)__cvta_generic_to_shared(Oc);
-    // MASKIN: per ring slot, bit q = "list entry q of this thread is a fixed DOF"
-    unsigned mring = 0u;
+    // MASKIN: FIFO of 4-bit masks (bit q = "list entry q of this thread is a fixed DOF"), one per staged plane
+    // in plane order: a plane's mask is pushed when its copies are issued and popped two steps later, when they
+    // have landed -- at fixed nibble positions (see the z-loop), so no variable shifts. flp: flags of the next
+    // plane to be staged (planes are staged in consecutive order).
+    unsigned pend = 0u;
+    const long long plane_nodes = (long long)G.px * G.py;
+    const uint8_t* flp = MASKIN ? P.fixed + plane_nodes * (kz0 - 1) : nullptr;
 
     // stage node plane k and occupancy layer k into ring slot sl (zero-filled outside the grid)
-    auto load_layer = [&](int k, int sl) {
+    auto load_layer = [&](int k, int sl, int nib) {  // nib: FIFO position of this plane's mask (MASKIN)
       if (k >= 0 && k < G.pz) {
         const char* src = reinterpret_cast<const char*>(P.u + plane_stride * k);
         const unsigned base = up_s + (unsigned)(8 * sl * PS);
@@ -250,25 +257,22 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
         for (int q = 0; q < kStage; ++q) e[q] = st_list[q * NT + t];
 #pragma unroll
         for (int q = 0; q < kStage; ++q)
-          if (q < ncnt) cp_async8_s(base + (unsigned)e[q].x, src + e[q].y);
+          if (q < ncnt) cp_async8_s(base + (MASKIN ? (unsigned)e[q].x & ~7u : (unsigned)e[q].x), src + e[q].y);
         if (MASKIN) {
-          const uint8_t* fl = P.fixed + (long long)G.px * G.py * k;
           unsigned bits = 0u;
 #pragma unroll
           for (int q = 0; q < kStage; ++q)
-            if (q < ncnt) {
-              const int gd = e[q].y / 8;  // in-plane double: node gd / 3, axis gd % 3
-              bits |= ((unsigned)(fl[gd / 3] >> (gd % 3)) & 1u) << q;
-            }
-          mring = (mring & ~(15u << (4 * sl))) | (bits << (4 * sl));
+            if (q < ncnt)  // node = in-plane byte offset / 24, axis from the entry's low bits
+              bits |= (((unsigned)flp[(unsigned)e[q].y / 24u] >> ((unsigned)e[q].x & 3u)) & 1u) << q;
+          pend |= bits << (4 * nib);
         }
       } else {  // halo plane above / below the grid (first / last piece only)
         double* dst = Up + sl * PS;
 #pragma unroll
         for (int q = 0; q < kStage; ++q)
           if (q < ncnt) dst[st_list[q * NT + t].x / 8] = 0.0;
-        if (MASKIN) mring &= ~(15u << (4 * sl));
       }
+      if (MASKIN) flp += plane_nodes;
       if (has_occ) {
         if (k >= 0 && k < G.nz) cp_async8_s(oc_s + (unsigned)(8 * sl * OS) + ooff, P.occ + layer_stride * k + oeoff);
         else Oc[sl * OS + ooff / 8] = 0.0;
@@ -286,9 +290,8 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
     };
 
     // MASKIN: clear this thread's fixed staged doubles of ring slot sl (after they landed)
-    auto apply_mask = [&](int sl) {
+    auto apply_mask = [&](int sl, unsigned bits) {
       if (!MASKIN) return;
-      const unsigned bits = (mring >> (4 * sl)) & 15u;
       if (bits == 0u) return;
       double* dst = Up + sl * PS;
 #pragma unroll
@@ -309,7 +312,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
     // sk = ring slot of plane / layer k; plane k+1 sits in sk+1, plane k+kAhead in sk-1 (mod kRing)
     auto step = [&](int k, int sk, const double (&bot)[12], double (&top)[12]) {
       const int sk1 = sk == kRing - 1 ? 0 : sk + 1, skl = sk == 0 ? kRing - 1 : sk - 1;
-      if (k + kAhead <= kz1 && !(TVB_MV_DBG(P) & 2)) load_layer(k + kAhead, skl);
+      if (k + kAhead <= kz1 && !(TVB_MV_DBG(P) & 2)) load_layer(k + kAhead, skl, 2);  // FIFO: [k+2, k+3] pending
       else cp_async_commit();  // keep one group per step
       gather_face(sk1, top);
       xy_forward(top);
@@ -351,7 +354,10 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
         for (int a = 0; a < 3; ++a) uo[a] = Up[sk * PS + j00 + S + 3 + a];
       }
       cp_async_wait_group<kAhead - 2>();  // plane k+2 (and occupancy k+2) landed
-      if (MASKIN && k + 2 <= kz1) apply_mask(sk == kRing - 2 ? 0 : (sk == kRing - 1 ? 1 : sk + 2));
+      if (MASKIN) {  // pop plane k+2's mask
+        if (k + 2 <= kz1) apply_mask(sk == kRing - 2 ? 0 : (sk == kRing - 1 ? 1 : sk + 2), pend & 15u);
+        pend >>= 4;
+      }
       if (!(TVB_MV_DBG(P) & 1)) __syncthreads();
       if (out) {
         // node (x0+tx, y0+ty) = local (1,1) of this column, (0,1) of column
@@ -388,14 +394,16 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(MatvecParams P, Modal M) {
     };
 
     const int s0 = (kz0 - 1 + kRing) % kRing;  // slot of the first staged plane kz0 - 1
+#pragma unroll
     for (int j = 0; j < kAhead; ++j) {
-      if (kz0 - 1 + j <= kz1) load_layer(kz0 - 1 + j, (s0 + j) % kRing);
+      if (kz0 - 1 + j <= kz1) load_layer(kz0 - 1 + j, (s0 + j) % kRing, j);
       else cp_async_commit();
     }
     cp_async_wait_group<kAhead - 2>();
-    if (MASKIN) {  // planes kz0 - 1 and kz0 landed
-      apply_mask(s0);
-      apply_mask(s0 == kRing - 1 ? 0 : s0 + 1);
+    if (MASKIN) {  // planes kz0 - 1 and kz0 landed: pop their masks
+      apply_mask(s0, pend & 15u);
+      apply_mask(s0 == kRing - 1 ? 0 : s0 + 1, (pend >> 4) & 15u);
+      pend >>= 8;
     }
     __syncthreads();
     double fa[12], fb[12];
@@ -500,6 +508,10 @@ static void set_smem_attr(size_t bytes) {
     cudaFuncSetAttribute(k_matvec<NT, MINB, true, false, 0, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     cudaFuncSetAttribute(k_matvec<NT, MINB, true, true, 0, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   }
+  if (WX != 0) {  // fused input mask with constant geometry (no-dot variants)
+    cudaFuncSetAttribute(k_matvec<NT, MINB, false, false, WX, WY, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(k_matvec<NT, MINB, false, true, WX, WY, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  }
   cudaFuncSetAttribute(k_matvec<NT, MINB, false, false, WX, WY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   cudaFuncSetAttribute(k_matvec<NT, MINB, false, true, WX, WY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   cudaFuncSetAttribute(k_matvec<NT, MINB, true, false, WX, WY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -509,7 +521,12 @@ static void set_smem_attr(size_t bytes) {
 template <int NT, int MINB, int WX = 0, int WY = 0>
 static void launch_nt(dim3 grid, size_t smem, cudaStream_t s, const MatvecParams& P, const Modal& M) {
   const bool dot = P.dot_partial != nullptr, mo = P.mask_out && P.fixed != nullptr;
-  if (P.mask_in && P.fixed != nullptr) {  // fused input mask: runtime-shape kernel
+  if (P.mask_in && P.fixed != nullptr) {  // fused input mask (with the dot epilogue: runtime-shape kernel only)
+    if (!dot && WX != 0) {
+      if (mo) launch_k(k_matvec<NT, MINB, false, true, WX, WY, true>, grid, NT, smem, s, P, M);
+      else launch_k(k_matvec<NT, MINB, false, false, WX, WY, true>, grid, NT, smem, s, P, M);
+      return;
+    }
     if (dot && mo) launch_k(k_matvec<NT, MINB, true, true, 0, 0, true>, grid, NT, smem, s, P, M);
     else if (dot) launch_k(k_matvec<NT, MINB, true, false, 0, 0, true>, grid, NT, smem, s, P, M);
     else if (mo) launch_k(k_matvec<NT, MINB, false, true, 0, 0, true>, grid, NT, smem, s, P, M);
@@ -526,7 +543,7 @@ static void launch_nt(dim3 grid, size_t smem, cudaStream_t s, const MatvecParams
 // BASELINE grids (C2 23x11, C4 25x10, C5 28x9, C1 / C3 42x6)
 static bool launch_fixed_shape(const MatvecPlan& pl, dim3 grid, cudaStream_t s, const MatvecParams& P, const Modal& M) {
   static const bool off = getenv("TVB_MV_GENERIC") != nullptr;
-  if (off || pl.nt != 256 || (P.mask_in && P.fixed != nullptr) || P.accumulate) return false;
+  if (off || pl.nt != 256 || P.accumulate) return false;
 #define TVB_SHAPE(X, Y)                                  \
   if (pl.wx == X && pl.wy == Y) {                        \
     launch_nt<256, 2, X, Y>(grid, pl.smem, s, P, M);     \
